@@ -1,0 +1,127 @@
+/*
+ * bida_gpu.h — C-ABI of the B200 batched heuristic evaluator.
+ *
+ * This is the drop-in boundary for the reference's evaluator backend
+ * (/root/reference/proj/include/bida/batch_eval.hpp:45-51,
+ *  `EvaluatorBackend<D>::evaluate(span<const BatchItem<D>>, span<int32_t>)`).
+ * Plain pointers and sizes only; no C++ or torch types.  The C++ adapter
+ * `bida_gpu::GpuBackend<D>` (include/bida_gpu_backend.hpp) wraps it into a
+ * `bida::EvaluatorBackend<D>`; INTEGRATION.md shows the bindings.
+ *
+ * States cross the boundary PACKED exactly as the reference packs them:
+ *   STP N=2..4 : one little-endian u64, 4 bits per cell (stp.hpp:121-126)
+ *   Rubik's    : {u64 lo, u64 hi} = RubiksCube::Packed (rubiks.hpp:121-137)
+ * The one-hot encode (stp.hpp:141-146, rubiks.hpp:155-166) happens on the
+ * device, so the backend reports needs_features() == false.
+ *
+ * Every entry point returns a status (BIDA_OK == 0); on failure the message
+ * is available from bida_gpu_last_error() (thread-local).  Nothing throws.
+ * Handles are safe to use from several host threads at once (the agent thread
+ * and evaluate_single / evaluate_sync callers of batch_eval.hpp:241,261).
+ */
+#ifndef BIDA_GPU_H
+#define BIDA_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BIDA_GPU_ABI_VERSION 1
+
+/* Domains: TilePuzzle<N> (stp.hpp:19-286) and RubiksCube (rubiks.hpp:19-383). */
+enum bida_domain {
+    BIDA_DOMAIN_STP2 = 2,
+    BIDA_DOMAIN_STP3 = 3,
+    BIDA_DOMAIN_STP4 = 4,
+    BIDA_DOMAIN_RC = 100
+};
+
+/* Status codes.  INVALID_ARGUMENT / RUNTIME mirror the std::invalid_argument /
+ * std::runtime_error the reference throws from the same call. */
+enum bida_status {
+    BIDA_OK = 0,
+    BIDA_ERR_INVALID_ARGUMENT = 1, /* ctor checks, batch_eval.hpp:87-93       */
+    BIDA_ERR_RUNTIME = 2,          /* BLIN1 load errors, batch_eval.hpp:111-129 */
+    BIDA_ERR_CUDA = 3,             /* device / driver failure                 */
+    BIDA_ERR_DISTRIBUTION = 4,     /* ClassDistribution::validate, heuristic.hpp:95-104 */
+    BIDA_ERR_STATE = 5,            /* packed state encodes outside [0, F)     */
+    BIDA_ERR_CAPACITY = 6          /* batch larger than the handle allows     */
+};
+
+enum bida_model_kind { BIDA_MODEL_LINEAR = 1, BIDA_MODEL_MLP = 2 };
+
+typedef struct bida_gpu_evaluator bida_gpu_evaluator;
+
+typedef struct bida_gpu_model_info {
+    int32_t kind;           /* bida_model_kind                 */
+    int32_t domain;         /* bida_domain                     */
+    int32_t features;       /* F = D::feature_length()         */
+    int32_t classes;        /* C                               */
+    int32_t ensemble;       /* E                               */
+    int32_t hidden_layers;  /* MLP only, else 0                */
+    int32_t hidden[8];      /* MLP widths                      */
+    double quantile;        /* q of quantile_class             */
+    int32_t device;
+    int32_t weights_in_smem;
+} bida_gpu_model_info;
+
+int bida_gpu_abi_version(void);
+const char *bida_gpu_last_error(void);
+int bida_gpu_device_count(void);
+/* D::feature_length() (stp.hpp:139, rubiks.hpp:153); -1 for unknown domain. */
+int bida_gpu_feature_length(int domain);
+/* bytes of one packed state (8 or 16); -1 for unknown domain. */
+int bida_gpu_packed_bytes(int domain);
+
+/* LinearModelBackend(member_weights, classes, quantile) (batch_eval.hpp:85-94).
+ * weights: ensemble * classes * F floats, member-major, each member row-major
+ * [C][F] as in the reference.  q is validated here (the reference validates it
+ * in quantile_class, heuristic.hpp:110-111, at evaluate time). */
+int bida_gpu_linear_create(int device, int domain, const float *weights, int ensemble,
+                           int classes, double quantile, bida_gpu_evaluator **out);
+
+/* LinearModelBackend::load(path, quantile) (batch_eval.hpp:109-131) from an
+ * in-memory BLIN1 image, and from a file path with the reference's messages. */
+int bida_gpu_linear_create_blin1(int device, int domain, const void *blob, size_t len,
+                                 double quantile, bida_gpu_evaluator **out);
+int bida_gpu_linear_load(int device, int domain, const char *path, double quantile,
+                         bida_gpu_evaluator **out);
+
+/* BMLP1 integer MLP ensemble (project format; the reference has
+ * no MLP).  Same readout as the linear model. */
+int bida_gpu_mlp_create_bmlp1(int device, int domain, const void *blob, size_t len,
+                              double quantile, bida_gpu_evaluator **out);
+int bida_gpu_mlp_load(int device, int domain, const char *path, double quantile,
+                      bida_gpu_evaluator **out);
+
+/* EvaluatorBackend<D>::evaluate (batch_eval.hpp:49): n packed HOST states ->
+ * n int32 h-values in HOST memory.  Synchronous; any n >= 0 (batches larger
+ * than the internal staging are pipelined in chunks).  On error every h_out[i]
+ * is still written (0). */
+int bida_gpu_evaluate(bida_gpu_evaluator *ev, const void *packed, int64_t n, int32_t *h_out);
+
+/* Same, also returning the per-member logits as float64 [n][E][C]
+ * (diagnostics / parity; may be NULL). */
+int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t n,
+                             int32_t *h_out, double *logits_out);
+
+/* Device-resident variant: d_packed / d_h / d_logits are DEVICE pointers on
+ * the handle's device, `stream` a cudaStream_t (NULL = legacy default).
+ * Asynchronous: returns after enqueueing; call bida_gpu_stream_status() after
+ * synchronising the stream to collect a deferred per-state error. */
+int bida_gpu_evaluate_device(bida_gpu_evaluator *ev, const void *d_packed, int64_t n,
+                             int32_t *d_h, double *d_logits, void *stream);
+int bida_gpu_stream_status(bida_gpu_evaluator *ev);
+
+int bida_gpu_info(const bida_gpu_evaluator *ev, bida_gpu_model_info *out);
+/* Number of kernel launches issued by this handle so far (bench evidence). */
+int64_t bida_gpu_launch_count(const bida_gpu_evaluator *ev);
+int bida_gpu_destroy(bida_gpu_evaluator *ev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BIDA_GPU_H */

@@ -1,0 +1,577 @@
+// bida_gpu.cu — host side of the C-ABI (include/bida_gpu.h) and kernel
+// dispatch.  One handle = one model resident on one device, plus a pair of
+// pinned staging slots and streams so host<->device copies of chunk i+1
+// overlap the kernel of chunk i.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <iterator>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/bida_gpu.h"
+#include "common.cuh"
+#include "linear.cuh"
+#include "mlp.cuh"
+
+using namespace bida_gpu;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                             \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(BIDA_ERR_CUDA, std::string(#expr " failed: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+int feature_length(int domain) {
+    switch (domain) {
+    case BIDA_DOMAIN_STP2: return 16;
+    case BIDA_DOMAIN_STP3: return 81;
+    case BIDA_DOMAIN_STP4: return 256;
+    case BIDA_DOMAIN_RC: return 480;
+    default: return -1;
+    }
+}
+int packed_bytes(int domain) {
+    if (domain == BIDA_DOMAIN_RC)
+        return 16;
+    return feature_length(domain) > 0 ? 8 : -1;
+}
+
+} // namespace
+
+struct bida_gpu_evaluator {
+    int kind = 0, domain = 0, F = 0, C = 0, E = 0, device = 0;
+    double q = 0.5, thr = 0.0;
+    int num_sms = 148;
+
+    // linear model
+    float *d_Wt = nullptr;
+    uint8_t *d_rowflag = nullptr;
+    int any_rowflag = 0;
+    int w_in_smem = 0;
+    size_t lin_smem = 0;
+    int lin_grid_cap = 0;
+
+    // MLP model
+    MlpModel *mlp = nullptr;
+    int hidden_layers = 0;
+    int hidden[8] = {0};
+
+    std::mutex mu;
+    cudaStream_t stream[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    int64_t slot_cap = 0;
+    void *h_in[2] = {nullptr, nullptr};
+    int32_t *h_h[2] = {nullptr, nullptr};
+    void *d_in[2] = {nullptr, nullptr};
+    int32_t *d_h[2] = {nullptr, nullptr};
+    int *err_host = nullptr; // mapped pinned, kErrWords ints
+    int *err_dev = nullptr;
+    std::atomic<int64_t> launches{0};
+};
+
+namespace {
+
+constexpr int64_t kMaxSlot = int64_t(1) << 20;
+
+template <int DOMAIN, int CS>
+int launch_linear_t(bida_gpu_evaluator *ev, const LinearArgs &a, cudaStream_t st) {
+    auto kern = linear_eval_kernel<DOMAIN, CS>;
+    if (ev->lin_smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(ev->lin_smem)));
+    const int64_t groups = (a.n + 31) / 32;
+    const int64_t want = (groups + kLinearWarps - 1) / kLinearWarps;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, ev->lin_grid_cap)));
+    kern<<<grid, kLinearThreads, ev->lin_smem, st>>>(a);
+    ev->launches.fetch_add(1, std::memory_order_relaxed);
+    CUDA_TRY(cudaGetLastError());
+    return BIDA_OK;
+}
+
+template <int DOMAIN>
+int launch_linear_d(bida_gpu_evaluator *ev, const LinearArgs &a, cudaStream_t st) {
+    const int cs = (ev->C + 31) / 32;
+    switch (cs) {
+    case 1: return launch_linear_t<DOMAIN, 1>(ev, a, st);
+    case 2: return launch_linear_t<DOMAIN, 2>(ev, a, st);
+    case 3: return launch_linear_t<DOMAIN, 3>(ev, a, st);
+    case 4: return launch_linear_t<DOMAIN, 4>(ev, a, st);
+    default: return launch_linear_t<DOMAIN, 8>(ev, a, st);
+    }
+}
+
+int launch(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h, double *d_logits,
+           cudaStream_t st) {
+    if (n <= 0)
+        return BIDA_OK;
+    if (ev->kind == BIDA_MODEL_MLP)
+        return mlp_launch(ev->mlp, ev->domain, d_packed, n, d_h, d_logits, ev->err_dev, st,
+                          &ev->launches)
+                   ? fail(BIDA_ERR_CUDA, mlp_last_error())
+                   : BIDA_OK;
+    LinearArgs a;
+    a.packed = d_packed;
+    a.n = n;
+    a.h_out = d_h;
+    a.logits_out = d_logits;
+    a.Wt = ev->d_Wt;
+    a.rowflag = ev->d_rowflag;
+    a.E = ev->E;
+    a.C = ev->C;
+    a.thr = ev->thr;
+    a.w_in_smem = ev->w_in_smem;
+    a.any_rowflag = ev->any_rowflag;
+    a.err = ev->err_dev;
+    switch (ev->domain) {
+    case BIDA_DOMAIN_STP2: return launch_linear_d<kSTP2>(ev, a, st);
+    case BIDA_DOMAIN_STP3: return launch_linear_d<kSTP3>(ev, a, st);
+    case BIDA_DOMAIN_STP4: return launch_linear_d<kSTP4>(ev, a, st);
+    default: return launch_linear_d<kRC>(ev, a, st);
+    }
+}
+
+int collect_errors(bida_gpu_evaluator *ev) {
+    volatile int *e = ev->err_host;
+    int rc = BIDA_OK;
+    if (e[kErrState])
+        rc = fail(BIDA_ERR_STATE, "packed state encodes a feature outside [0, F)");
+    else if (e[kErrDistribution])
+        rc = fail(BIDA_ERR_DISTRIBUTION, "ClassDistribution: probabilities must sum to 1");
+    for (int k = 0; k < kErrWords; ++k)
+        e[k] = 0;
+    return rc;
+}
+
+int ensure_slots(bida_gpu_evaluator *ev, int64_t n) {
+    const int64_t want = std::min<int64_t>(std::max<int64_t>(n, 1024), kMaxSlot);
+    if (ev->slot_cap >= want)
+        return BIDA_OK;
+    int64_t cap = 1024;
+    while (cap < want)
+        cap <<= 1;
+    const int pb = packed_bytes(ev->domain);
+    for (int s = 0; s < 2; ++s) {
+        if (ev->h_in[s]) cudaFreeHost(ev->h_in[s]);
+        if (ev->h_h[s]) cudaFreeHost(ev->h_h[s]);
+        if (ev->d_in[s]) cudaFree(ev->d_in[s]);
+        if (ev->d_h[s]) cudaFree(ev->d_h[s]);
+        ev->h_in[s] = ev->h_h[s] = nullptr;
+        ev->d_in[s] = ev->d_h[s] = nullptr;
+        CUDA_TRY(cudaHostAlloc(&ev->h_in[s], cap * pb, cudaHostAllocDefault));
+        CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&ev->h_h[s]), cap * 4, cudaHostAllocDefault));
+        CUDA_TRY(cudaMalloc(&ev->d_in[s], cap * pb));
+        CUDA_TRY(cudaMalloc(reinterpret_cast<void **>(&ev->d_h[s]), cap * 4));
+    }
+    ev->slot_cap = cap;
+    return BIDA_OK;
+}
+
+int common_init(bida_gpu_evaluator *ev, int device) {
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "device index out of range");
+    ev->device = device;
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(BIDA_ERR_CUDA, std::string("this library is built for sm_100a (B200); device is ") +
+                                       prop.name);
+    ev->num_sms = prop.multiProcessorCount;
+    for (int s = 0; s < 2; ++s) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&ev->stream[s], cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&ev->done[s], cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&ev->err_host), kErrWords * sizeof(int),
+                           cudaHostAllocMapped));
+    std::memset(ev->err_host, 0, kErrWords * sizeof(int));
+    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&ev->err_dev), ev->err_host, 0));
+    return BIDA_OK;
+}
+
+void release(bida_gpu_evaluator *ev) {
+    if (!ev)
+        return;
+    cudaSetDevice(ev->device);
+    for (int s = 0; s < 2; ++s) {
+        if (ev->stream[s]) cudaStreamSynchronize(ev->stream[s]);
+        if (ev->h_in[s]) cudaFreeHost(ev->h_in[s]);
+        if (ev->h_h[s]) cudaFreeHost(ev->h_h[s]);
+        if (ev->d_in[s]) cudaFree(ev->d_in[s]);
+        if (ev->d_h[s]) cudaFree(ev->d_h[s]);
+        if (ev->done[s]) cudaEventDestroy(ev->done[s]);
+        if (ev->stream[s]) cudaStreamDestroy(ev->stream[s]);
+    }
+    if (ev->err_host) cudaFreeHost(ev->err_host);
+    if (ev->d_Wt) cudaFree(ev->d_Wt);
+    if (ev->d_rowflag) cudaFree(ev->d_rowflag);
+    if (ev->mlp) mlp_destroy(ev->mlp);
+    delete ev;
+}
+
+int check_quantile(double q) {
+    if (!(q > 0.0 && q <= 1.0))
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "quantile_class: q must be in (0, 1]");
+    return BIDA_OK;
+}
+
+bool read_file(const char *path, std::vector<unsigned char> &out) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f)
+        return false;
+    out.assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+    return true;
+}
+
+uint32_t rd_u32(const unsigned char *b) {
+    return uint32_t(b[0]) | uint32_t(b[1]) << 8 | uint32_t(b[2]) << 16 | uint32_t(b[3]) << 24;
+}
+
+int linear_create_impl(int device, int domain, const float *weights, int E, int C, double q,
+                       bida_gpu_evaluator **out) {
+    if (!out)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "out handle pointer is NULL");
+    *out = nullptr;
+    const int F = feature_length(domain);
+    if (F < 0)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "unknown domain");
+    if (E <= 0)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "LinearModelBackend: empty ensemble");
+    if (C <= 0)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "LinearModelBackend: need at least one class");
+    if (C > kMaxClasses)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "classes > 256 are not supported by the GPU readout");
+    if (!weights)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "LinearModelBackend: weight matrix size mismatch");
+    if (int rc = check_quantile(q))
+        return rc;
+
+    auto *ev = new bida_gpu_evaluator();
+    ev->kind = BIDA_MODEL_LINEAR;
+    ev->domain = domain;
+    ev->F = F;
+    ev->C = C;
+    ev->E = E;
+    ev->q = q;
+    ev->thr = q - 1e-12;
+    if (int rc = common_init(ev, device)) {
+        release(ev);
+        return rc;
+    }
+    // Transpose [E][C][F] -> [E][F][C] so class lanes read consecutive floats.
+    const size_t nw = static_cast<size_t>(E) * F * C;
+    std::vector<float> wt(nw);
+    std::vector<uint8_t> flag(static_cast<size_t>(E) * C, 0);
+    for (int m = 0; m < E; ++m)
+        for (int c = 0; c < C; ++c)
+            for (int j = 0; j < F; ++j) {
+                const float w = weights[(static_cast<size_t>(m) * C + c) * F + j];
+                wt[(static_cast<size_t>(m) * F + j) * C + c] = w;
+                if (!std::isfinite(w)) {
+                    flag[static_cast<size_t>(m) * C + c] = 1;
+                    ev->any_rowflag = 1;
+                }
+            }
+    auto bail = [&](int rc) {
+        release(ev);
+        return rc;
+    };
+    {
+        cudaError_t e = cudaMalloc(&ev->d_Wt, nw * sizeof(float));
+        if (e == cudaSuccess)
+            e = cudaMemcpy(ev->d_Wt, wt.data(), nw * sizeof(float), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess)
+            e = cudaMalloc(&ev->d_rowflag, flag.size());
+        if (e == cudaSuccess)
+            e = cudaMemcpy(ev->d_rowflag, flag.data(), flag.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess)
+            return bail(fail(BIDA_ERR_CUDA, std::string("weight upload: ") + cudaGetErrorString(e)));
+    }
+    const int cpad = (C + 1) & ~1;
+    const size_t extra = static_cast<size_t>(kLinearWarps) * cpad * 8 + kLinearWarps * 32 * 4;
+    const size_t wbytes = (nw * 4 + 15) & ~size_t(15);
+    ev->w_in_smem = (wbytes + extra <= 200 * 1024) ? 1 : 0;
+    ev->lin_smem = (ev->w_in_smem ? wbytes : 0) + extra;
+    // Resident CTAs per SM from the smem budget (228 KB/SM, 1 KB reserved per CTA).
+    const size_t per_cta = ev->lin_smem + 1024;
+    int per_sm = static_cast<int>(std::min<size_t>(8, (228 * 1024) / per_cta));
+    per_sm = std::max(per_sm, 1);
+    ev->lin_grid_cap = ev->num_sms * per_sm;
+    *out = ev;
+    return BIDA_OK;
+}
+
+int parse_blin1(const unsigned char *b, size_t len, int F, const std::string &name,
+                std::vector<float> &w, int &C, int &E) {
+    if (len < 5 || std::memcmp(b, "BLIN1", 5) != 0)
+        return fail(BIDA_ERR_RUNTIME, "not a BLIN1 file: " + name);
+    if (len < 17)
+        return fail(BIDA_ERR_RUNTIME, "BLIN1 header does not match domain: " + name);
+    const uint32_t flen = rd_u32(b + 5), classes = rd_u32(b + 9), ens = rd_u32(b + 13);
+    if (flen != static_cast<uint32_t>(F) || ens == 0)
+        return fail(BIDA_ERR_RUNTIME, "BLIN1 header does not match domain: " + name);
+    const size_t count = static_cast<size_t>(flen) * classes * ens;
+    if (len < 17 + count * 4)
+        return fail(BIDA_ERR_RUNTIME, "truncated BLIN1 file: " + name);
+    w.resize(count);
+    std::memcpy(w.data(), b + 17, count * 4);
+    C = static_cast<int>(classes);
+    E = static_cast<int>(ens);
+    return BIDA_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int bida_gpu_abi_version(void) { return BIDA_GPU_ABI_VERSION; }
+const char *bida_gpu_last_error(void) { return g_last_error.c_str(); }
+
+int bida_gpu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess)
+        return 0;
+    return n;
+}
+
+int bida_gpu_feature_length(int domain) { return feature_length(domain); }
+int bida_gpu_packed_bytes(int domain) { return packed_bytes(domain); }
+
+int bida_gpu_linear_create(int device, int domain, const float *weights, int ensemble, int classes,
+                           double quantile, bida_gpu_evaluator **out) {
+    return linear_create_impl(device, domain, weights, ensemble, classes, quantile, out);
+}
+
+int bida_gpu_linear_create_blin1(int device, int domain, const void *blob, size_t len,
+                                 double quantile, bida_gpu_evaluator **out) {
+    if (out)
+        *out = nullptr;
+    const int F = feature_length(domain);
+    if (F < 0)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "unknown domain");
+    std::vector<float> w;
+    int C = 0, E = 0;
+    if (int rc = parse_blin1(static_cast<const unsigned char *>(blob), blob ? len : 0, F,
+                             "<memory>", w, C, E))
+        return rc;
+    return linear_create_impl(device, domain, w.data(), E, C, quantile, out);
+}
+
+int bida_gpu_linear_load(int device, int domain, const char *path, double quantile,
+                         bida_gpu_evaluator **out) {
+    if (out)
+        *out = nullptr;
+    const int F = feature_length(domain);
+    if (F < 0)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "unknown domain");
+    std::vector<unsigned char> buf;
+    if (!path || !read_file(path, buf))
+        return fail(BIDA_ERR_RUNTIME, std::string("cannot open weights file: ") + (path ? path : ""));
+    std::vector<float> w;
+    int C = 0, E = 0;
+    if (int rc = parse_blin1(buf.data(), buf.size(), F, path, w, C, E))
+        return rc;
+    return linear_create_impl(device, domain, w.data(), E, C, quantile, out);
+}
+
+int bida_gpu_mlp_create_bmlp1(int device, int domain, const void *blob, size_t len,
+                              double quantile, bida_gpu_evaluator **out) {
+    if (!out)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "out handle pointer is NULL");
+    *out = nullptr;
+    const int F = feature_length(domain);
+    if (F < 0)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "unknown domain");
+    if (int rc = check_quantile(quantile))
+        return rc;
+    auto *ev = new bida_gpu_evaluator();
+    ev->kind = BIDA_MODEL_MLP;
+    ev->domain = domain;
+    ev->F = F;
+    ev->q = quantile;
+    ev->thr = quantile - 1e-12;
+    if (int rc = common_init(ev, device)) {
+        release(ev);
+        return rc;
+    }
+    MlpShape shape;
+    std::string err;
+    const int rc = mlp_create(static_cast<const unsigned char *>(blob), blob ? len : 0, F,
+                              ev->thr, ev->num_sms, &ev->mlp, &shape, &err);
+    if (rc) {
+        release(ev);
+        return fail(rc, err);
+    }
+    ev->C = shape.C;
+    ev->E = shape.E;
+    ev->hidden_layers = shape.L;
+    for (int l = 0; l < shape.L && l < 8; ++l)
+        ev->hidden[l] = shape.H[l];
+    *out = ev;
+    return BIDA_OK;
+}
+
+int bida_gpu_mlp_load(int device, int domain, const char *path, double quantile,
+                      bida_gpu_evaluator **out) {
+    if (out)
+        *out = nullptr;
+    std::vector<unsigned char> buf;
+    if (!path || !read_file(path, buf))
+        return fail(BIDA_ERR_RUNTIME, std::string("cannot open weights file: ") + (path ? path : ""));
+    return bida_gpu_mlp_create_bmlp1(device, domain, buf.data(), buf.size(), quantile, out);
+}
+
+int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t n, int32_t *h_out,
+                             double *logits_out) {
+    if (!ev)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL evaluator");
+    if (n < 0 || (n > 0 && (!packed || !h_out)))
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "bad batch arguments");
+    if (n == 0)
+        return BIDA_OK;
+    std::lock_guard<std::mutex> lk(ev->mu);
+    CUDA_TRY(cudaSetDevice(ev->device));
+    if (int rc = ensure_slots(ev, n)) {
+        std::fill(h_out, h_out + n, 0);
+        return rc;
+    }
+    const int pb = packed_bytes(ev->domain);
+    const size_t per_logits = static_cast<size_t>(ev->E) * ev->C;
+    double *d_logits = nullptr;
+    if (logits_out)
+        CUDA_TRY(cudaMalloc(&d_logits, static_cast<size_t>(std::min<int64_t>(n, ev->slot_cap)) *
+                                           per_logits * sizeof(double)));
+    const char *src = static_cast<const char *>(packed);
+    int64_t pend_off[2] = {-1, -1}, pend_n[2] = {0, 0};
+    int rc = BIDA_OK;
+    auto drain = [&](int s) -> int {
+        if (pend_off[s] < 0)
+            return BIDA_OK;
+        cudaError_t e = cudaEventSynchronize(ev->done[s]);
+        if (e != cudaSuccess)
+            return fail(BIDA_ERR_CUDA, std::string("evaluate: ") + cudaGetErrorString(e));
+        std::memcpy(h_out + pend_off[s], ev->h_h[s], pend_n[s] * 4);
+        pend_off[s] = -1;
+        return BIDA_OK;
+    };
+    int slot = 0;
+    for (int64_t i0 = 0; i0 < n && rc == BIDA_OK; i0 += ev->slot_cap, slot ^= 1) {
+        const int64_t m = std::min<int64_t>(ev->slot_cap, n - i0);
+        if ((rc = drain(slot)))
+            break;
+        std::memcpy(ev->h_in[slot], src + i0 * pb, m * pb);
+        cudaStream_t st = ev->stream[slot];
+        cudaError_t e = cudaMemcpyAsync(ev->d_in[slot], ev->h_in[slot], m * pb,
+                                        cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) {
+            rc = fail(BIDA_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e));
+            break;
+        }
+        if ((rc = launch(ev, ev->d_in[slot], m, ev->d_h[slot], d_logits, st)))
+            break;
+        e = cudaMemcpyAsync(ev->h_h[slot], ev->d_h[slot], m * 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess)
+            e = cudaEventRecord(ev->done[slot], st);
+        if (e != cudaSuccess) {
+            rc = fail(BIDA_ERR_CUDA, std::string("D2H: ") + cudaGetErrorString(e));
+            break;
+        }
+        pend_off[slot] = i0;
+        pend_n[slot] = m;
+        if (d_logits) {
+            // diagnostics path: serialise so the single logits buffer is reused safely
+            e = cudaMemcpyAsync(logits_out + i0 * per_logits, d_logits,
+                                m * per_logits * sizeof(double), cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess)
+                e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) {
+                rc = fail(BIDA_ERR_CUDA, std::string("logits D2H: ") + cudaGetErrorString(e));
+                break;
+            }
+        }
+    }
+    for (int s = 0; s < 2; ++s) {
+        const int r = drain(slot ^ s ^ 1) ? BIDA_ERR_CUDA : BIDA_OK;
+        if (rc == BIDA_OK)
+            rc = r;
+    }
+    // make sure no stream still writes staging before we return
+    cudaStreamSynchronize(ev->stream[0]);
+    cudaStreamSynchronize(ev->stream[1]);
+    if (d_logits)
+        cudaFree(d_logits);
+    if (rc != BIDA_OK) {
+        std::fill(h_out, h_out + n, 0);
+        collect_errors(ev);
+        return rc;
+    }
+    return collect_errors(ev);
+}
+
+int bida_gpu_evaluate(bida_gpu_evaluator *ev, const void *packed, int64_t n, int32_t *h_out) {
+    return bida_gpu_evaluate_logits(ev, packed, n, h_out, nullptr);
+}
+
+int bida_gpu_evaluate_device(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h,
+                             double *d_logits, void *stream) {
+    if (!ev)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL evaluator");
+    if (n < 0 || (n > 0 && (!d_packed || !d_h)))
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "bad batch arguments");
+    CUDA_TRY(cudaSetDevice(ev->device));
+    return launch(ev, d_packed, n, d_h, d_logits, static_cast<cudaStream_t>(stream));
+}
+
+int bida_gpu_stream_status(bida_gpu_evaluator *ev) {
+    if (!ev)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL evaluator");
+    return collect_errors(ev);
+}
+
+int bida_gpu_info(const bida_gpu_evaluator *ev, bida_gpu_model_info *out) {
+    if (!ev || !out)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL argument");
+    std::memset(out, 0, sizeof(*out));
+    out->kind = ev->kind;
+    out->domain = ev->domain;
+    out->features = ev->F;
+    out->classes = ev->C;
+    out->ensemble = ev->E;
+    out->hidden_layers = ev->hidden_layers;
+    for (int l = 0; l < 8; ++l)
+        out->hidden[l] = ev->hidden[l];
+    out->quantile = ev->q;
+    out->device = ev->device;
+    out->weights_in_smem = ev->w_in_smem;
+    return BIDA_OK;
+}
+
+int64_t bida_gpu_launch_count(const bida_gpu_evaluator *ev) {
+    return ev ? ev->launches.load(std::memory_order_relaxed) : 0;
+}
+
+int bida_gpu_destroy(bida_gpu_evaluator *ev) {
+    release(ev);
+    return BIDA_OK;
+}
+
+} // extern "C"
