@@ -35,6 +35,9 @@ WORKLOADS = {
     "rc-linear-e1-c21": dict(domain="rc", kind="linear", E=1, C=21, q=0.5, batch=1 << 22),
     "rc-linear-e4-c21": dict(domain="rc", kind="linear", E=4, C=21, q=0.5, batch=1 << 22),
     "stp4-linear-c72": dict(domain="stp4", kind="linear", E=1, C=72, q=0.5, batch=1 << 22),
+    # BMLP1 int8 MLPs; widths bracket the paper's 0.2 / 2.3 MB model-size anchors
+    "rc-mlp-h128": dict(domain="rc", kind="mlp", H=[128, 128], E=1, C=21, q=0.5, batch=1 << 22),
+    "rc-mlp-h512": dict(domain="rc", kind="mlp", H=[512, 512], E=1, C=21, q=0.5, batch=1 << 22),
 }
 DEFAULT_WORKLOAD = "rc-linear-e1-c21"
 
@@ -69,55 +72,61 @@ def algorithmic(wl):
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    def __init__(self, device: int):
-        self.device = device
-        self.proc = None
-        self.lines = []
+    """Samples SM clock and clock-event (throttle) reasons through NVML every
+    `period` seconds while the timed region runs (the recipe's clocks line)."""
+
+    def __init__(self, device: int, period: float = 0.005):
+        self.device, self.period = device, period
+        self.samples = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device),
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.ok = True
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.ok = False
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+                try:
+                    bits = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    bits = N.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.samples.append((sm, bits))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.ok:
+            self.t.join(1)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 4:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-                bits = int(parts[3], 16)
-            except ValueError:
-                continue
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        reasons = set()
+        for _, bits in self.samples:
             for b, name in THROTTLE_BITS.items():
                 if bits & b and name != "gpu_idle":
                     reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        sm = [s for s, _ in self.samples]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(sm), "source": "NVML, 5 ms period, device-timed + e2e regions"}
 
 
 # ---------------------------------------------------------- dist helpers
@@ -195,14 +204,14 @@ def run_ours(args, wl, rank, world, local):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        t_start.record(stream)
-        for i in range(args.steps):
-            ev[i][0].record(stream)
-            be.evaluate_device(d_in[i % nbuf], d_h[i % nbuf])
-            ev[i][1].record(stream)
-        t_end.record(stream)
-        torch.cuda.synchronize()
+    clk = ClockSampler(local).__enter__()
+    t_start.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        be.evaluate_device(d_in[i % nbuf], d_h[i % nbuf])
+        ev[i][1].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
     be.status()
     launches = be.launch_count() - launches0
     barrier(world)
@@ -225,6 +234,7 @@ def run_ours(args, wl, rank, world, local):
         out[:] = be.evaluate(hostbufs[i % len(hostbufs)])
     e2e_s = time.perf_counter() - t0
     barrier(world)
+    clk.__exit__(None, None, None)
     e2e_s_max = reduce_max(e2e_s, world)
     clocks = clk.summary()
     be.close()

@@ -1,0 +1,163 @@
+// bida_gpu_backend.hpp — C++ drop-in for the reference's evaluator backend.
+//
+//   bida::EvaluatorBackend<D>  (/root/reference/proj/include/bida/batch_eval.hpp:45-51)
+//     virtual void evaluate(std::span<const BatchItem<D>>, std::span<std::int32_t>) = 0;
+//     virtual bool needs_features() const;
+//
+// GpuBackend<D> implements it over the C-ABI in bida_gpu.h, so the
+// reference's Evaluator / EvaluatorGroup / batch_idastar / aidastar use the
+// B200 evaluator unchanged:
+//
+//   std::vector<std::unique_ptr<bida::EvaluatorBackend<D>>> backends;
+//   for (int g = 0; g < n_gpus; ++g)
+//       backends.push_back(bida_gpu::GpuBackend<D>::load_linear(g, "w.blin", 0.5));
+//   bida::EvaluatorGroup<D> group(std::move(backends), batch, timeout_us);
+//
+// Contract: needs_features() is false — states are packed
+// with the reference's own D::pack and one-hot encoded on the device; every
+// out[i] is written; evaluate() never throws (an exception on the agent thread
+// would std::terminate), errors are counted and the last message kept.
+// Construction errors throw std::invalid_argument / std::runtime_error like
+// LinearModelBackend's constructor and load() (batch_eval.hpp:87-93, 111-129).
+// Calls may come concurrently from the agent thread and evaluate_single /
+// evaluate_sync callers; the C-ABI handle is re-entrant.
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <fstream>
+#include <iterator>
+#include <memory>
+#include <mutex>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "bida/batch_eval.hpp"
+#include "bida/rubiks.hpp"
+#include "bida/stp.hpp"
+#include "bida_gpu.h"
+
+namespace bida_gpu {
+
+template <class D>
+struct DomainOf;
+template <int N>
+struct DomainOf<bida::TilePuzzle<N>> {
+    static constexpr int id = N;  // BIDA_DOMAIN_STP2..4
+    static constexpr int packed_bytes = 8;
+    static void pack(const typename bida::TilePuzzle<N>::State &s, unsigned char *out) {
+        const std::uint64_t v = bida::TilePuzzle<N>::pack(s);  // stp.hpp:121-126
+        std::memcpy(out, &v, 8);
+    }
+};
+template <>
+struct DomainOf<bida::RubiksCube> {
+    static constexpr int id = BIDA_DOMAIN_RC;
+    static constexpr int packed_bytes = 16;
+    static void pack(const bida::RubiksCube::State &s, unsigned char *out) {
+        const bida::RubiksCube::Packed p = bida::RubiksCube::pack(s);  // rubiks.hpp:126-137
+        std::memcpy(out, &p.lo, 8);
+        std::memcpy(out + 8, &p.hi, 8);
+    }
+};
+
+inline void throw_status(int rc, const char *what) {
+    const std::string msg = std::string(what) + ": " + bida_gpu_last_error();
+    if (rc == BIDA_ERR_INVALID_ARGUMENT)
+        throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+template <class D>
+class GpuBackend final : public bida::EvaluatorBackend<D> {
+public:
+    using Traits = DomainOf<D>;
+
+    // LinearModelBackend(member_weights, classes, quantile) on `device`.
+    GpuBackend(int device, const std::vector<std::vector<float>> &member_weights, int classes,
+               double quantile) {
+        if (member_weights.empty())
+            throw std::invalid_argument("LinearModelBackend: empty ensemble");
+        const std::size_t per = static_cast<std::size_t>(classes) * D::feature_length();
+        std::vector<float> flat;
+        for (const auto &w : member_weights) {
+            if (w.size() != per)
+                throw std::invalid_argument("LinearModelBackend: weight matrix size mismatch");
+            flat.insert(flat.end(), w.begin(), w.end());
+        }
+        bida_gpu_evaluator *h = nullptr;
+        const int rc = bida_gpu_linear_create(device, Traits::id, flat.data(),
+                                              static_cast<int>(member_weights.size()), classes, quantile, &h);
+        if (rc)
+            throw_status(rc, "GpuBackend");
+        handle_ = h;
+    }
+
+    // LinearModelBackend::load(path, quantile) (BLIN1) on `device`.
+    static std::unique_ptr<GpuBackend> load_linear(int device, const std::string &path, double quantile) {
+        bida_gpu_evaluator *h = nullptr;
+        const int rc = bida_gpu_linear_load(device, Traits::id, path.c_str(), quantile, &h);
+        if (rc)
+            throw_status(rc, "GpuBackend::load_linear");
+        return std::unique_ptr<GpuBackend>(new GpuBackend(h));
+    }
+
+    // BMLP1 integer MLP ensemble on `device`.
+    static std::unique_ptr<GpuBackend> load_mlp(int device, const std::string &path, double quantile) {
+        bida_gpu_evaluator *h = nullptr;
+        const int rc = bida_gpu_mlp_load(device, Traits::id, path.c_str(), quantile, &h);
+        if (rc)
+            throw_status(rc, "GpuBackend::load_mlp");
+        return std::unique_ptr<GpuBackend>(new GpuBackend(h));
+    }
+
+    ~GpuBackend() override {
+        if (handle_)
+            bida_gpu_destroy(handle_);
+    }
+    GpuBackend(const GpuBackend &) = delete;
+    GpuBackend &operator=(const GpuBackend &) = delete;
+
+    bool needs_features() const override { return false; }
+
+    void evaluate(std::span<const bida::BatchItem<D>> batch, std::span<std::int32_t> out) override {
+        thread_local std::vector<unsigned char> staging;
+        const std::size_t n = batch.size();
+        staging.resize(n * Traits::packed_bytes);
+        for (std::size_t i = 0; i < n; ++i)
+            Traits::pack(batch[i].state, staging.data() + i * Traits::packed_bytes);
+        const int rc = bida_gpu_evaluate(handle_, staging.data(), static_cast<std::int64_t>(n), out.data());
+        calls_.fetch_add(1, std::memory_order_relaxed);
+        items_.fetch_add(n, std::memory_order_relaxed);
+        if (rc) {
+            for (auto &v : out)
+                v = 0;  // h >= 0 keeps frames from blocking forever (cbdfs.hpp:262-265)
+            errors_.fetch_add(1, std::memory_order_relaxed);
+            std::lock_guard<std::mutex> lk(err_m_);
+            last_error_ = bida_gpu_last_error();
+        }
+    }
+
+    std::uint64_t errors() const { return errors_.load(std::memory_order_relaxed); }
+    std::uint64_t calls() const { return calls_.load(std::memory_order_relaxed); }
+    std::uint64_t items() const { return items_.load(std::memory_order_relaxed); }
+    std::string last_error() const {
+        std::lock_guard<std::mutex> lk(err_m_);
+        return last_error_;
+    }
+    bida_gpu_evaluator *handle() const { return handle_; }
+
+private:
+    explicit GpuBackend(bida_gpu_evaluator *h) : handle_(h) {}
+
+    bida_gpu_evaluator *handle_ = nullptr;
+    std::atomic<std::uint64_t> errors_{0}, calls_{0}, items_{0};
+    mutable std::mutex err_m_;
+    std::string last_error_;
+};
+
+} // namespace bida_gpu

@@ -1,0 +1,126 @@
+"""GPU parity of the tcgen05 BMLP1 evaluator against the oracle's BMLP1
+restatement (oracle/bida_oracle.c), through the C-ABI.  Integer logits are
+exact, so the bar is bit-exact logits and h on every state; the certified
+float32 readout must agree with the float64 reference sequence everywhere,
+including the ties that force its exact replay."""
+import numpy as np
+import pytest
+
+import paper_2507_11916_b200 as bida
+from oracle_lib import RC, STP2, STP3, STP4, Oracle
+from paper_2507_11916_b200.models import BMLP1, Layer, make_bmlp1
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle()
+
+
+def check(orc, domain, blob, q, packed, E, C):
+    with bida.MlpModelBackend(domain, blob, q) as be:
+        h, lg = be.evaluate_logits(packed)
+        h2 = be.evaluate(packed)
+    ho, lo = orc.mlp_evaluate(blob, domain, q, packed, want_logits=True, E=E, Cc=C, threads=8)
+    assert np.array_equal(lg.view(np.uint64), lo.view(np.uint64)), "logits differ"
+    assert (h == ho).all(), f"{(h != ho).sum()} h flips"
+    assert (h2 == ho).all()
+    return h
+
+
+@pytest.mark.parametrize(
+    "domain,hidden,C,E,q",
+    [
+        (RC, [128, 128], 21, 1, 0.5),
+        (RC, [128, 128], 21, 2, 0.3),
+        (RC, [512, 512], 21, 1, 0.5),
+        (RC, [256], 27, 1, 0.9),
+        (RC, [64, 96, 128], 40, 3, 0.5),
+        (STP4, [256, 256], 72, 1, 0.5),
+        (STP4, [128], 64, 2, 1.0),
+        (STP3, [64, 64], 32, 1, 0.5),
+        (STP2, [32], 7, 1, 0.05),
+    ],
+)
+def test_mlp_matches_oracle(orc, domain, hidden, C, E, q):
+    blob = make_bmlp1(domain, hidden=hidden, classes=C, ensemble=E, seed=sum(hidden) + C)
+    packed = bida.random_walks(domain, 1000, 0, 40, seed=C)
+    h = check(orc, domain, blob, q, packed, E, C)
+    assert len(np.unique(h)) > 1
+
+
+def test_ragged_and_empty(orc):
+    blob = make_bmlp1("rc", hidden=[128, 128], classes=21, ensemble=1, seed=3)
+    packed = bida.random_walks("rc", 700, 0, 30, seed=4)
+    want = orc.mlp_evaluate(blob, RC, 0.5, packed, threads=8)
+    with bida.MlpModelBackend("rc", blob, 0.5) as be:
+        assert len(be.evaluate(packed[:0])) == 0
+        for n in (1, 127, 128, 129, 255, 256, 257, 700):
+            assert (be.evaluate(packed[:n]) == want[:n]).all(), n
+
+
+def test_ties_force_exact_replay(orc):
+    """All-zero weights: uniform softmax, cum hits q exactly at class C*q-1 —
+    undecidable in float32, so every state takes the float64 replay."""
+    m = BMLP1(480, 4, [32])
+    layers = [Layer(np.zeros((32, 480), np.int8), np.zeros(32, np.int32), 0),
+              Layer(np.zeros((4, 32), np.int8), np.zeros(4, np.int32), 0)]
+    m.members.append((layers, 1.0))
+    blob = m.to_bytes()
+    packed = bida.random_walks("rc", 300, 0, 20, seed=1)
+    for q in (0.25, 0.5, 0.75, 1.0, 0.3):
+        h = check(orc, RC, blob, q, packed, 1, 4)
+        assert len(np.unique(h)) == 1
+
+
+def test_saturated_logits(orc):
+    """Huge out_scale: logits ~1e6 -> float32 bound gives up, exact path decides."""
+    blob = make_bmlp1("rc", hidden=[64], classes=21, ensemble=1, seed=9, logit_std=5e5)
+    packed = bida.random_walks("rc", 400, 0, 30, seed=2)
+    check(orc, RC, blob, 0.5, packed, 1, 21)
+
+
+def test_large_batch_composition(orc):
+    blob = make_bmlp1("rc", hidden=[256, 256], classes=21, ensemble=1, seed=11)
+    n = (1 << 20) + 333
+    packed = bida.random_walks("rc", n, 0, 30, seed=12)
+    with bida.MlpModelBackend("rc", blob, 0.5) as be:
+        h = be.evaluate(packed)
+        sample = np.arange(0, n, 509)
+        assert (h[sample] == orc.mlp_evaluate(blob, RC, 0.5, packed[sample], threads=8)).all()
+        parts = np.concatenate([be.evaluate(packed[i : i + 77777]) for i in range(0, 400000, 77777)])
+        assert (parts == h[: len(parts)]).all()
+
+
+def test_malformed_state_is_an_error():
+    blob = make_bmlp1("rc", hidden=[64], classes=21, ensemble=1, seed=1)
+    bad = np.zeros(3, bida.instances.packed_dtype("rc"))
+    bad["hi"][1] = np.uint64(0xFFFFFFFFFFFF)
+    with bida.MlpModelBackend("rc", blob, 0.5) as be:
+        with pytest.raises(ValueError, match="outside"):
+            be.evaluate(bad)
+        good = bida.random_walks("rc", 5, 0, 5, seed=1)
+        assert (be.evaluate(good) >= 0).all()
+
+
+def test_device_resident(orc):
+    torch = pytest.importorskip("torch")
+    blob = make_bmlp1("rc", hidden=[128, 128], classes=21, ensemble=1, seed=21)
+    packed = bida.random_walks("rc", 5000, 0, 30, seed=22)
+    d_in = torch.from_numpy(packed.view(np.uint8).copy()).cuda()
+    d_h = torch.empty(len(packed), dtype=torch.int32, device="cuda")
+    with bida.MlpModelBackend("rc", blob, 0.5) as be:
+        be.evaluate_device(d_in, d_h)
+        torch.cuda.synchronize()
+        be.status()
+    assert (d_h.cpu().numpy() == orc.mlp_evaluate(blob, RC, 0.5, packed, threads=8)).all()
+
+
+def test_bad_models_rejected():
+    with pytest.raises(ValueError):
+        bida.MlpModelBackend("rc", make_bmlp1("rc", hidden=[100], classes=21, seed=1), 0.5)  # not /32
+    with pytest.raises(RuntimeError):
+        bida.MlpModelBackend("rc", b"BMLP1" + b"\0" * 8, 0.5)
+    with pytest.raises(RuntimeError):
+        bida.MlpModelBackend("stp4", make_bmlp1("rc", hidden=[64], classes=21, seed=1), 0.5)
