@@ -47,7 +47,8 @@ def test_mlp_matches_oracle(orc, domain, hidden, C, E, q):
     blob = make_bmlp1(domain, hidden=hidden, classes=C, ensemble=E, seed=sum(hidden) + C)
     packed = bida.random_walks(domain, 1000, 0, 40, seed=C)
     h = check(orc, domain, blob, q, packed, E, C)
-    assert len(np.unique(h)) > 1
+    if q < 0.99:  # at q = 1 every state correctly reads out the top class
+        assert len(np.unique(h)) > 1
 
 
 def test_ragged_and_empty(orc):
