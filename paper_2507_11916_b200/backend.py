@@ -45,10 +45,17 @@ class _GpuBackendBase:
         """The GPU encodes on the device from packed states."""
         return False
 
-    def evaluate(self, packed) -> np.ndarray:
-        """h-values (int32) for a batch of packed states (batch_eval.hpp:49)."""
+    def evaluate(self, packed, out: np.ndarray | None = None) -> np.ndarray:
+        """h-values (int32) for a batch of packed states (batch_eval.hpp:49).
+        `out` (optional, int32[n]) receives the result; page-locked host
+        buffers on either side are transferred by DMA without staging."""
         p = _as_packed(self.domain, packed)
-        h = np.empty(len(p), np.int32)
+        if out is None:
+            h = np.empty(len(p), np.int32)
+        else:
+            h = out
+            if h.dtype != np.int32 or not h.flags["C_CONTIGUOUS"] or len(h) != len(p):
+                raise ValueError("out must be a contiguous int32 array of the batch length")
         if len(p):
             _native.check(
                 _native.lib().bida_gpu_evaluate(self._h, p.ctypes.data_as(C.c_void_p), len(p),

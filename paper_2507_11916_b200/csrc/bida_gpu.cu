@@ -228,6 +228,15 @@ void release(bida_gpu_evaluator *ev) {
     delete ev;
 }
 
+bool is_pinned(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 int check_quantile(double q) {
     if (!(q > 0.0 && q <= 1.0))
         return fail(BIDA_ERR_INVALID_ARGUMENT, "quantile_class: q must be in (0, 1]");
@@ -461,6 +470,11 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         CUDA_TRY(cudaMalloc(&d_logits, static_cast<size_t>(std::min<int64_t>(n, ev->slot_cap)) *
                                            per_logits * sizeof(double)));
     const char *src = static_cast<const char *>(packed);
+    // Caller buffers that are already page-locked (cudaHostAlloc /
+    // cudaHostRegister / torch pin_memory) are DMA'd directly; pageable ones
+    // go through the handle's pinned staging slots.
+    const bool in_pinned = is_pinned(packed);
+    const bool out_pinned = is_pinned(h_out);
     int64_t pend_off[2] = {-1, -1}, pend_n[2] = {0, 0};
     int rc = BIDA_OK;
     auto drain = [&](int s) -> int {
@@ -469,7 +483,8 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         cudaError_t e = cudaEventSynchronize(ev->done[s]);
         if (e != cudaSuccess)
             return fail(BIDA_ERR_CUDA, std::string("evaluate: ") + cudaGetErrorString(e));
-        std::memcpy(h_out + pend_off[s], ev->h_h[s], pend_n[s] * 4);
+        if (!out_pinned)
+            std::memcpy(h_out + pend_off[s], ev->h_h[s], pend_n[s] * 4);
         pend_off[s] = -1;
         return BIDA_OK;
     };
@@ -478,17 +493,21 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         const int64_t m = std::min<int64_t>(ev->slot_cap, n - i0);
         if ((rc = drain(slot)))
             break;
-        std::memcpy(ev->h_in[slot], src + i0 * pb, m * pb);
+        const void *h2d_src = src + i0 * pb;
+        if (!in_pinned) {
+            std::memcpy(ev->h_in[slot], src + i0 * pb, m * pb);
+            h2d_src = ev->h_in[slot];
+        }
         cudaStream_t st = ev->stream[slot];
-        cudaError_t e = cudaMemcpyAsync(ev->d_in[slot], ev->h_in[slot], m * pb,
-                                        cudaMemcpyHostToDevice, st);
+        cudaError_t e = cudaMemcpyAsync(ev->d_in[slot], h2d_src, m * pb, cudaMemcpyHostToDevice, st);
         if (e != cudaSuccess) {
             rc = fail(BIDA_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e));
             break;
         }
         if ((rc = launch(ev, ev->d_in[slot], m, ev->d_h[slot], d_logits, st)))
             break;
-        e = cudaMemcpyAsync(ev->h_h[slot], ev->d_h[slot], m * 4, cudaMemcpyDeviceToHost, st);
+        e = cudaMemcpyAsync(out_pinned ? static_cast<void *>(h_out + i0) : static_cast<void *>(ev->h_h[slot]),
+                            ev->d_h[slot], m * 4, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess)
             e = cudaEventRecord(ev->done[slot], st);
         if (e != cudaSuccess) {

@@ -37,29 +37,32 @@
 namespace bida_gpu {
 
 constexpr int kMaxMembers = 8;
-constexpr int kMaxLayers = 5;  // hidden layers <= 4
+constexpr int kMaxLayers = 5;   // hidden layers <= 4
 constexpr int kTileM = 128;
-constexpr int kStages = 4;
-constexpr int kMlpThreads = 192;
-constexpr int kKChunk = 32;  // bytes of K per MMA / per weight stage
+constexpr int kMaxStages = 6;
+constexpr int kStageBytes = 16384;
+constexpr int kMlpThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2-9 two epilogue groups
+constexpr int kKChunk = 32;       // bytes of K per MMA instruction
 
 struct MlpLayer {
     int K, N;          // padded input width (multiple of 32), output width (multiple of 16)
     int shift;         // hidden layers
-    int boff;          // bias offset (int32 elements)
+    int boff;          // bias offset (int32 elements, multiple of 4)
     long long woff;    // weight image offset (bytes)
 };
 
 struct MlpParams {
     const uint8_t *wimg;
     const int32_t *bias;
-    int E, nl, C, Kmax, Nmax, Fpad;
+    int E, nl, C, Fpad;
     MlpLayer layer[kMaxMembers][kMaxLayers];
     float scale_f[kMaxMembers];
     double scale_d[kMaxMembers];
     ReadoutConsts rk;
     uint32_t tmem_cols;
-    int stage_bytes;
+    int slots;          // 2: two tiles in flight (ping-pong); 1: both groups split one tile's columns
+    int stages;         // weight ring depth (16 KB stages)
+    int xbytes, ybytes; // activation buffers per slot (even / odd layer inputs)
     // batch
     const void *packed;
     long long n;
@@ -81,33 +84,46 @@ namespace {
 thread_local std::string g_err;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// K-chunks (32 B of K each) carried by one 16 KB stage for a layer with N outputs.
+__device__ __forceinline__ int chunks_per_stage(int N) {
+    const int c = kStageBytes / (N * kKChunk);
+    return c < 1 ? 1 : c;
+}
 } // namespace
 
+// One CTA per SM, persistent over the CTA's tiles of 128 states.  Local tile
+// k of this CTA is t = blockIdx.x + k * gridDim.x; with two slots, tiles
+// alternate between slot 0 and 1 (epilogue group g owns slot g), and the MMA
+// issuer interleaves the slots layer by layer so one slot's tensor-core work
+// overlaps the other slot's epilogue.
 template <int DOMAIN, int CM>
 __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_constant__ MlpParams p) {
     using T = DomainTraits<DOMAIN>;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int act_bytes = kTileM * p.Kmax;
-    uint8_t *bufX = smem;
-    uint8_t *bufY = smem + act_bytes;
-    uint8_t *stages = smem + 2 * act_bytes;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(stages + kStages * p.stage_bytes);
-    uint64_t *full = bars;                   // [kStages]
-    uint64_t *empty = bars + kStages;        // [kStages]
-    uint64_t *act_ready = bars + 2 * kStages;
-    uint64_t *d_full = act_ready + 1;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(d_full + 1);
+    const int slot_bytes = p.xbytes + p.ybytes;
+    uint8_t *stages = smem + p.slots * slot_bytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stages + p.stages * kStageBytes);
+    uint64_t *full = bars;                       // [kMaxStages]
+    uint64_t *empty = bars + kMaxStages;         // [kMaxStages]
+    uint64_t *act_ready = bars + 2 * kMaxStages; // [2]
+    uint64_t *d_full = act_ready + 2;            // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(d_full + 2);
 
     const int warp = threadIdx.x >> 5;
     const long long ntiles = (p.n + kTileM - 1) / kTileM;
+    const long long nloc = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const int slots = p.slots;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kMaxStages; ++s) {
             sm100::mbar_init(&full[s], 1);
             sm100::mbar_init(&empty[s], 1);
         }
-        sm100::mbar_init(act_ready, kTileM);
-        sm100::mbar_init(d_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            sm100::mbar_init(&act_ready[s], slots == 2 ? 128 : 256);
+            sm100::mbar_init(&d_full[s], 1);
+        }
         sm100::fence_barrier_init();
     }
     if (warp == 1)
@@ -122,71 +138,90 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
         if (lane_id() == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (long long t = blockIdx.x; t < ntiles; t += gridDim.x)
+            for (long long k0 = 0; k0 < nloc; k0 += slots)
                 for (int e = 0; e < p.E; ++e)
-                    for (int l = 0; l < p.nl; ++l) {
-                        const MlpLayer &ly = p.layer[e][l];
-                        const uint32_t bytes = static_cast<uint32_t>(ly.N) * kKChunk;
-                        const uint8_t *src = p.wimg + ly.woff;
-                        for (int kc = 0; kc < ly.K / kKChunk; ++kc) {
-                            sm100::mbar_wait(&empty[s], ph ^ 1u);
-                            sm100::mbar_arrive_expect_tx(&full[s], bytes);
-                            sm100::bulk_g2s(stages + s * p.stage_bytes, src + static_cast<size_t>(kc) * bytes,
-                                            bytes, &full[s]);
-                            if (++s == kStages) {
-                                s = 0;
-                                ph ^= 1u;
+                    for (int l = 0; l < p.nl; ++l)
+                        for (int sl = 0; sl < slots && k0 + sl < nloc; ++sl) {
+                            const MlpLayer &ly = p.layer[e][l];
+                            const int nch = ly.K / kKChunk, cps = chunks_per_stage(ly.N);
+                            const uint32_t cbytes = static_cast<uint32_t>(ly.N) * kKChunk;
+                            for (int kc = 0; kc < nch; kc += cps) {
+                                const int cnt = min(cps, nch - kc);
+                                sm100::mbar_wait(&empty[s], ph ^ 1u);
+                                sm100::mbar_arrive_expect_tx(&full[s], cnt * cbytes);
+                                sm100::bulk_g2s(stages + s * kStageBytes, p.wimg + ly.woff + static_cast<size_t>(kc) * cbytes,
+                                                cnt * cbytes, &full[s]);
+                                if (++s == p.stages) {
+                                    s = 0;
+                                    ph ^= 1u;
+                                }
                             }
                         }
-                    }
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
         if (lane_id() == 0) {
             int s = 0;
-            uint32_t ph = 0, aph = 0;
-            const uint32_t sX = sm100::smem_u32(bufX), sY = sm100::smem_u32(bufY);
-            const uint32_t sS = sm100::smem_u32(stages);
-            for (long long t = blockIdx.x; t < ntiles; t += gridDim.x)
+            uint32_t ph = 0, aph[2] = {0u, 0u};
+            const uint32_t sbase = sm100::smem_u32(smem), sS = sm100::smem_u32(stages);
+            for (long long k0 = 0; k0 < nloc; k0 += slots)
                 for (int e = 0; e < p.E; ++e)
-                    for (int l = 0; l < p.nl; ++l) {
-                        const MlpLayer &ly = p.layer[e][l];
-                        sm100::mbar_wait(act_ready, aph);
-                        aph ^= 1u;
-                        sm100::tc_fence_after();
-                        const uint32_t abase = (l & 1) ? sY : sX;
-                        const uint32_t lbo_b = static_cast<uint32_t>(ly.N) * 16u;
-                        for (int kc = 0; kc < ly.K / kKChunk; ++kc) {
-                            sm100::mbar_wait(&full[s], ph);
+                    for (int l = 0; l < p.nl; ++l)
+                        for (int sl = 0; sl < slots && k0 + sl < nloc; ++sl) {
+                            const MlpLayer &ly = p.layer[e][l];
+                            sm100::mbar_wait(&act_ready[sl], aph[sl]);
+                            aph[sl] ^= 1u;
                             sm100::tc_fence_after();
-                            const uint64_t adesc = sm100::make_smem_desc(abase + kc * 4096u, 2048u, 128u);
-                            const uint32_t sbase = sS + s * p.stage_bytes;
-                            for (int n0 = 0; n0 < ly.N; n0 += 256) {
-                                const uint32_t nn = min(256, ly.N - n0);
-                                const uint64_t bdesc = sm100::make_smem_desc(sbase + (n0 / 8) * 128u, lbo_b, 128u);
-                                sm100::mma_i8(tmem + n0, adesc, bdesc, sm100::make_idesc_i8(nn), kc > 0 ? 1u : 0u);
+                            const uint32_t abase = sbase + sl * slot_bytes + ((l & 1) ? p.xbytes : 0);
+                            const uint32_t dcol = tmem + sl * 256u;
+                            const uint32_t lbo_b = static_cast<uint32_t>(ly.N) * 16u;
+                            const int nch = ly.K / kKChunk, cps = chunks_per_stage(ly.N);
+                            const uint32_t idesc_full = sm100::make_idesc_i8(ly.N < 256 ? ly.N : 256);
+                            for (int kc = 0; kc < nch; kc += cps) {
+                                const int cnt = min(cps, nch - kc);
+                                sm100::mbar_wait(&full[s], ph);
+                                sm100::tc_fence_after();
+                                const uint32_t stg = sS + s * kStageBytes;
+                                for (int j = 0; j < cnt; ++j) {
+                                    const uint64_t adesc = sm100::make_smem_desc(abase + (kc + j) * 4096u, 2048u, 128u);
+                                    const uint32_t cb = stg + j * static_cast<uint32_t>(ly.N) * kKChunk;
+                                    for (int n0 = 0; n0 < ly.N; n0 += 256) {
+                                        const int nn = ly.N - n0 < 256 ? ly.N - n0 : 256;
+                                        const uint64_t bdesc = sm100::make_smem_desc(cb + (n0 / 8) * 128u, lbo_b, 128u);
+                                        sm100::mma_i8(dcol + n0, adesc, bdesc,
+                                                      nn == 256 ? idesc_full : sm100::make_idesc_i8(nn),
+                                                      (kc + j) > 0 ? 1u : 0u);
+                                    }
+                                }
+                                sm100::mma_commit(&empty[s]);
+                                if (++s == p.stages) {
+                                    s = 0;
+                                    ph ^= 1u;
+                                }
                             }
-                            sm100::mma_commit(&empty[s]);
-                            if (++s == kStages) {
-                                s = 0;
-                                ph ^= 1u;
-                            }
+                            sm100::mma_commit(&d_full[sl]);
                         }
-                        sm100::mma_commit(d_full);
-                    }
         }
     } else {
         // ------------------------------------------------ encode / epilogue / readout
+        const int grp = (warp - 2) >> 2;           // epilogue group 0 / 1
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
         const int row = quad * 32 + lane_id();     // tile row == TMEM lane
-        const uint32_t t_row = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-        const uint32_t sX = sm100::smem_u32(bufX), sY = sm100::smem_u32(bufY);
+        const int sl = slots == 2 ? grp : 0;
+        const bool leader = slots == 2 || grp == 0;  // encodes, reads out, writes h
+        const uint32_t t_row = tmem + sl * 256u + (static_cast<uint32_t>(quad * 32) << 16);
+        const uint32_t sX = sm100::smem_u32(smem) + sl * slot_bytes;
+        const uint32_t sY = sX + p.xbytes;
+        uint64_t *my_ready = &act_ready[sl];
+        uint64_t *my_full = &d_full[sl];
         uint32_t dph = 0;
-        for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const long long kstep = slots == 2 ? 2 : 1;
+        for (long long k = (slots == 2 ? grp : 0); k < nloc; k += kstep) {
+            const long long t = blockIdx.x + k * gridDim.x;
             const long long st = t * kTileM + row;
             const bool valid = st < p.n;
             uint64_t lo = 0, hi = 0;
-            if (valid) {
+            if (valid && leader) {
                 if constexpr (T::PB == 16) {
                     const ulonglong2 v = reinterpret_cast<const ulonglong2 *>(p.packed)[st];
                     lo = v.x;
@@ -198,50 +233,58 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             int idx[T::NNZ];
             bool bad = false;
 #pragma unroll
-            for (int k = 0; k < T::NNZ; ++k) {
-                idx[k] = position_feature<DOMAIN>(lo, hi, k);
-                bad |= idx[k] < 0 || idx[k] >= T::F;
+            for (int q = 0; q < T::NNZ; ++q) {
+                idx[q] = position_feature<DOMAIN>(lo, hi, q);
+                bad |= idx[q] < 0 || idx[q] >= T::F;
             }
-            bad = bad && valid;
+            bad = bad && valid && leader;
             if (bad)
                 raise_error(p.err, kErrState);
             const bool live = valid && !bad;
             int hmin = 0x7fffffff;
             bool dist_bad = false;
             for (int e = 0; e < p.E; ++e) {
-                // ---- encode: one-hot row into X (layer 0's A operand)
-                for (int c16 = 0; c16 < p.Fpad / 16; ++c16)
-                    sm100::st_shared_v4(sX + c16 * 2048u + row * 16u, 0u, 0u, 0u, 0u);
-                if (live) {
+                if (leader) {
+                    // ---- encode: one-hot row into X (layer 0's A operand)
+                    for (int c16 = 0; c16 < p.Fpad / 16; ++c16)
+                        sm100::st_shared_v4(sX + c16 * 2048u + row * 16u, 0u, 0u, 0u, 0u);
+                    if (live) {
 #pragma unroll
-                    for (int k = 0; k < T::NNZ; ++k) {
-                        const int j = idx[k];
-                        sm100::st_shared_u8(sX + (j >> 4) * 2048u + row * 16u + (j & 15), 1u);
+                        for (int q = 0; q < T::NNZ; ++q) {
+                            const int j = idx[q];
+                            sm100::st_shared_u8(sX + (j >> 4) * 2048u + row * 16u + (j & 15), 1u);
+                        }
                     }
+                    sm100::fence_proxy_async_smem();
                 }
-                sm100::fence_proxy_async_smem();
-                sm100::mbar_arrive(act_ready);
+                sm100::mbar_arrive(my_ready);
                 for (int l = 0; l < p.nl; ++l) {
                     const MlpLayer &ly = p.layer[e][l];
-                    sm100::mbar_wait(d_full, dph);
+                    sm100::mbar_wait(my_full, dph);
                     dph ^= 1u;
                     sm100::tc_fence_after();
                     const int32_t *bias = p.bias + ly.boff;
                     if (l + 1 < p.nl) {
-                        // hidden layer epilogue: int8 A operand of layer l+1
+                        // hidden layer epilogue: bias, shift, clamp -> int8 A operand of layer l+1
                         const uint32_t out = ((l + 1) & 1) ? sY : sX;
-                        for (int c0 = 0; c0 < ly.N; c0 += 16) {
+                        const int half = slots == 2 ? ly.N : ly.N / 2;
+                        const int c_beg = slots == 2 ? 0 : grp * half, c_end = c_beg + half;
+                        for (int c0 = c_beg; c0 < c_end; c0 += 16) {
                             int32_t r[16];
                             sm100::tmem_ld16(t_row + c0, r);
+                            int4 b4[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
                             sm100::tmem_wait_ld();
                             uint32_t w[4];
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
+                                const int bq[4] = {b4[q].x, b4[q].y, b4[q].z, b4[q].w};
                                 uint32_t packed4 = 0;
 #pragma unroll
                                 for (int b = 0; b < 4; ++b) {
-                                    const int j = q * 4 + b;
-                                    int v = (r[j] + __ldg(bias + c0 + j)) >> ly.shift;
+                                    int v = (r[q * 4 + b] + bq[b]) >> ly.shift;
                                     v = min(max(v, 0), 127);
                                     packed4 |= static_cast<uint32_t>(v) << (8 * b);
                                 }
@@ -251,8 +294,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                         }
                         sm100::tc_fence_before();
                         sm100::fence_proxy_async_smem();
-                        sm100::mbar_arrive(act_ready);
-                    } else {
+                        sm100::mbar_arrive(my_ready);
+                    } else if (leader) {
                         // output layer: exact integer logits -> certified readout
                         int32_t v[CM];
 #pragma unroll
@@ -278,10 +321,11 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                     }
                 }
             }
-            if (valid && dist_bad)
-                raise_error(p.err, kErrDistribution);
-            if (valid)
+            if (leader && valid) {
+                if (dist_bad)
+                    raise_error(p.err, kErrDistribution);
                 p.h_out[st] = (live && !dist_bad) ? hmin : 0;
+            }
         }
     }
 
@@ -371,11 +415,13 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     p.nl = nl;
     p.C = static_cast<int>(C);
     p.Fpad = Fpad;
-    p.Kmax = Fpad;
-    p.Nmax = Cpad;
-    for (int h : H) {
-        p.Kmax = std::max(p.Kmax, h);
-        p.Nmax = std::max(p.Nmax, h);
+    int KX = Fpad, KY = 0, Nmax = Cpad;  // KX: even-layer inputs, KY: odd-layer inputs
+    for (uint32_t l = 0; l < L; ++l) {
+        Nmax = std::max(Nmax, H[l]);
+        if ((l + 1) % 2 == 0)
+            KX = std::max(KX, H[l]);
+        else
+            KY = std::max(KY, H[l]);
     }
     std::vector<uint8_t> img;
     std::vector<int32_t> bias;
@@ -451,17 +497,36 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     const double eps64 = (4.0 * C + 16.0) * std::ldexp(1.0, -53);
     p.rk.uLo = std::nextafter(static_cast<float>(u - eps64), 0.0f);
     p.rk.uHi = std::nextafter(static_cast<float>(u + eps64), INFINITY);
-    uint32_t cols = 32;
-    while (cols < static_cast<uint32_t>(p.Nmax))
-        cols <<= 1;
-    p.tmem_cols = cols;
-    p.stage_bytes = p.Nmax * kKChunk;
-    m->cm = C <= 32 ? 32 : (C <= 64 ? 64 : 256);
-    m->smem = 2ull * kTileM * p.Kmax + static_cast<size_t>(kStages) * p.stage_bytes + 8 * (2 * kStages + 2) + 16;
-    if (m->smem > 227 * 1024) {
+    p.xbytes = kTileM * KX;
+    p.ybytes = kTileM * KY;
+    const size_t bar_bytes = 8 * (2 * kMaxStages + 4) + 16;
+    const size_t budget = 227 * 1024;
+    auto stages_for = [&](int slots) -> int {
+        const size_t act = static_cast<size_t>(slots) * (p.xbytes + p.ybytes);
+        if (act + bar_bytes + 2 * kStageBytes > budget)
+            return 0;
+        return static_cast<int>(std::min<size_t>(4, (budget - act - bar_bytes) / kStageBytes));
+    };
+    // Two tiles in flight when both accumulators fit TMEM (2 x 256 columns)
+    // and both slots' activation buffers fit shared memory; else one tile
+    // whose columns the two epilogue groups split.
+    if (Nmax <= 256 && stages_for(2) >= 2) {
+        p.slots = 2;
+        p.stages = stages_for(2);
+        p.tmem_cols = 512;
+    } else if (stages_for(1) >= 2) {
+        p.slots = 1;
+        p.stages = stages_for(1);
+        uint32_t cols = 32;
+        while (cols < static_cast<uint32_t>(Nmax))
+            cols <<= 1;
+        p.tmem_cols = cols;
+    } else {
         delete m;
         return fail(err, 1, "BMLP1: model too wide for shared memory");
     }
+    m->cm = C <= 32 ? 32 : (C <= 64 ? 64 : 256);
+    m->smem = static_cast<size_t>(p.slots) * (p.xbytes + p.ybytes) + static_cast<size_t>(p.stages) * kStageBytes + bar_bytes;
     m->grid_cap = num_sms;
     cudaError_t ce = cudaMalloc(&m->d_wimg, img.size());
     if (ce == cudaSuccess)
