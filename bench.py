@@ -154,6 +154,11 @@ def barrier(world):
         dist.barrier()
 
 
+def whole_job_rate(states_per_rank_step: int, steps: int, world: int, max_ms: float) -> float:
+    """Whole-job throughput: all ranks' states over the slowest rank's time."""
+    return states_per_rank_step * steps * world / (max_ms / 1000.0)
+
+
 def reduce_max(x: float, world: int) -> float:
     if world == 1:
         return x
@@ -373,7 +378,7 @@ def main():
         return
     B = r["B"]
     total_states = B * args.steps * world
-    value = total_states / (r["total_ms"] / 1000.0)
+    value = whole_job_rate(B, args.steps, world, r["total_ms"])
     by, fl = algorithmic(wl)
     import json as _json
 
