@@ -205,8 +205,8 @@ int orc_blin1_parse(const void *blob, size_t len, int F_expected, int *C, int *E
  *       u32 shift        (hidden layers only)
  *   and per member one f32 out_scale.
  *
- *   hidden: a'[o] = clamp((bias[o] + sum_i W[o][i]*a[i]) >> shift, 0, 127)
- *           (arithmetic shift = floor division by 2^shift; a is 0..127)
+ *   hidden: a'[o] = clamp((bias[o] + sum_i W[o][i]*a[i]) >> shift, 0, 255)
+ *           (arithmetic shift = floor division by 2^shift; a is u8 0..255)
  *   output: logit[c] = (double)(bias[c] + sum_i W[c][i]*a[i]) * (double)out_scale
  * followed by the reference readout (softmax, quantile_class, ensemble_min).
  * Layer 0's input is the one-hot encode (a = x in {0,1}).
@@ -313,7 +313,7 @@ static int mlp_eval_range(const orc_mlp *m, int domain, double q, const void *pa
                     for (int t = 0; t < ly->in; ++t) acc += (int32_t)w[t] * a[t];
                     if (l < m->L) {
                         int32_t v = acc >> ly->shift; /* arithmetic: floor division */
-                        nx[o] = v < 0 ? 0 : (v > 127 ? 127 : v);
+                        nx[o] = v < 0 ? 0 : (v > 255 ? 255 : v);
                     } else {
                         lg[o] = (double)acc * (double)m->out_scale[e];
                     }

@@ -59,6 +59,7 @@ int packed_bytes(int domain) {
 struct bida_gpu_evaluator {
     int kind = 0, domain = 0, F = 0, C = 0, E = 0, device = 0;
     double q = 0.5, thr = 0.0;
+    float uLo = 0.0f, uHi = 0.0f;
     int num_sms = 148;
 
     // linear model
@@ -137,6 +138,8 @@ int launch(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h
     a.E = ev->E;
     a.C = ev->C;
     a.thr = ev->thr;
+    a.uLo = ev->uLo;
+    a.uHi = ev->uHi;
     a.w_in_smem = ev->w_in_smem;
     a.any_rowflag = ev->any_rowflag;
     a.err = ev->err_dev;
@@ -282,6 +285,11 @@ int linear_create_impl(int device, int domain, const float *weights, int E, int 
     ev->E = E;
     ev->q = q;
     ev->thr = q - 1e-12;
+    {
+        const double u = 1.0 - ev->thr, eps64 = (4.0 * C + 16.0) * std::ldexp(1.0, -53);
+        ev->uLo = std::nextafter(static_cast<float>(u - eps64), 0.0f);
+        ev->uHi = std::nextafter(static_cast<float>(u + eps64), INFINITY);
+    }
     if (int rc = common_init(ev, device)) {
         release(ev);
         return rc;

@@ -71,29 +71,26 @@ template <int CM>
 __device__ __forceinline__ int readout_certified(const int32_t (&v)[CM], int C, float sf, double sd,
                                                  const ReadoutConsts &k, bool *bad, bool *fell_back) {
     constexpr float kLog2e = 1.4426950408889634f;
-    float l[CM];
     float m = -INFINITY, lam = 0.0f;
 #pragma unroll
     for (int c = 0; c < CM; ++c) {
         if (c < C) {
-            l[c] = static_cast<float>(v[c]) * sf;
-            m = fmaxf(m, l[c]);
-            lam = fmaxf(lam, fabsf(l[c]));
+            const float l = static_cast<float>(v[c]) * sf;
+            m = fmaxf(m, l);
+            lam = fmaxf(lam, fabsf(l));
         }
     }
     const float eta = 1.0e-6f * (lam + 1.0f);
     const float rho = 2.2f * (eta + static_cast<float>(C + 4) * 5.9604645e-8f);
     *fell_back = false;
     if (rho < 1.0e-2f) {  // false for NaN / inf / huge logits
-        float e[CM];
+        // e_c = exp(l_c - m), recomputed identically in both passes
+        auto ec = [&](int c) { return sm100::ex2_approx((static_cast<float>(v[c]) * sf - m) * kLog2e); };
         float Z = 0.0f;
 #pragma unroll
-        for (int c = 0; c < CM; ++c) {
-            if (c < C) {
-                e[c] = sm100::ex2_approx((l[c] - m) * kLog2e);
-                Z += e[c];
-            }
-        }
+        for (int c = 0; c < CM; ++c)
+            if (c < C)
+                Z += ec(c);
         const float A = k.uLo * Z * (1.0f - 2.1f * rho);
         const float B = k.uHi * Z * (1.0f + 2.1f * rho);
         float T = 0.0f;  // T_k = sum_{c > k} e_c
@@ -107,7 +104,7 @@ __device__ __forceinline__ int readout_certified(const int32_t (&v)[CM], int C, 
                     certified = T > B;
                     done = true;
                 } else {
-                    T += e[c];
+                    T += ec(c);
                 }
             }
         }

@@ -32,6 +32,7 @@ struct LinearArgs {
     const uint8_t *rowflag;  // [E][C]: row holds a non-finite weight
     int E, C;
     double thr;
+    float uLo, uHi;          // certified-readout thresholds (certified_readout.cuh)
     int w_in_smem;           // Wt copied to shared memory by every CTA
     int any_rowflag;
     int *err;                // mapped host error words
@@ -128,7 +129,7 @@ linear_eval_kernel(const LinearArgs a) {
                         if (a.logits_out && c < C)
                             a.logits_out[((base + k) * E + m) * C + c] = dot;
                     }
-                    const int h = warp_quantile_exact<CS>(lg, C, a.thr, scratch, lane, a.err);
+                    const int h = warp_quantile_certified<CS>(lg, C, a.thr, a.uLo, a.uHi, scratch, lane, a.err);
                     hmin = min(hmin, h);
                 }
             }

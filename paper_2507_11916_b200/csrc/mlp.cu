@@ -9,8 +9,8 @@
 //              and a weight k-chunk streamed by the producer warp with 1-D
 //              bulk async copies (TMA engine) into a 4-stage ring; int32
 //              accumulators live in TMEM
-//   epilogue : tcgen05.ld the accumulator rows, add bias, shift, clamp to
-//              0..127 and write the next layer's int8 A operand into the
+//   epilogue : tcgen05.ld the accumulator rows, add bias, shift, saturate to
+//              u8 0..255 and write the next layer's int8 A operand into the
 //              other activation buffer (fused activation / requantisation)
 //   readout  : last layer -> exact integer logits -> certified float32
 //              softmax/quantile (float64 replay when undecidable) -> min
@@ -216,20 +216,28 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
         uint64_t *my_full = &d_full[sl];
         uint32_t dph = 0;
         const long long kstep = slots == 2 ? 2 : 1;
+        // packed states are prefetched one tile ahead (HBM latency off the critical path)
+        auto load_state = [&](long long kk, uint64_t &lo_, uint64_t &hi_) {
+            lo_ = hi_ = 0;
+            const long long s_ = (blockIdx.x + kk * gridDim.x) * kTileM + row;
+            if (kk < nloc && s_ < p.n && leader) {
+                if constexpr (T::PB == 16) {
+                    const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2 *>(p.packed) + s_);
+                    lo_ = v.x;
+                    hi_ = v.y;
+                } else {
+                    lo_ = __ldcs(reinterpret_cast<const unsigned long long *>(p.packed) + s_);
+                }
+            }
+        };
+        uint64_t nlo, nhi;
+        load_state(slots == 2 ? grp : 0, nlo, nhi);
         for (long long k = (slots == 2 ? grp : 0); k < nloc; k += kstep) {
             const long long t = blockIdx.x + k * gridDim.x;
             const long long st = t * kTileM + row;
             const bool valid = st < p.n;
-            uint64_t lo = 0, hi = 0;
-            if (valid && leader) {
-                if constexpr (T::PB == 16) {
-                    const ulonglong2 v = reinterpret_cast<const ulonglong2 *>(p.packed)[st];
-                    lo = v.x;
-                    hi = v.y;
-                } else {
-                    lo = reinterpret_cast<const uint64_t *>(p.packed)[st];
-                }
-            }
+            const uint64_t lo = nlo, hi = nhi;
+            load_state(k + kstep, nlo, nhi);
             int idx[T::NNZ];
             bool bad = false;
 #pragma unroll
@@ -269,28 +277,43 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                         const uint32_t out = ((l + 1) & 1) ? sY : sX;
                         const int half = slots == 2 ? ly.N : ly.N / 2;
                         const int c_beg = slots == 2 ? 0 : grp * half, c_end = c_beg + half;
-                        for (int c0 = c_beg; c0 < c_end; c0 += 16) {
-                            int32_t r[16];
-                            sm100::tmem_ld16(t_row + c0, r);
-                            int4 b4[4];
+                        // software-pipelined: the TMEM load of the next 16 columns is in
+                        // flight while the current 16 are requantised and stored
+                        const int sh = ly.shift;
+                        auto requant = [&](const int32_t(&r)[16], const int4(&b4)[4], int c0) {
+                            uint32_t w[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)  // (acc + bias) >> shift, saturated to u8 0..255
+                                w[q] = sm100::pack_sat_u8x4((r[q * 4 + 0] + b4[q].x) >> sh, (r[q * 4 + 1] + b4[q].y) >> sh,
+                                                            (r[q * 4 + 2] + b4[q].z) >> sh, (r[q * 4 + 3] + b4[q].w) >> sh);
+                            sm100::st_shared_v4(out + (c0 >> 4) * 2048u + row * 16u, w[0], w[1], w[2], w[3]);
+                        };
+                        auto load_bias = [&](int4(&b4)[4], int c0) {
 #pragma unroll
                             for (int q = 0; q < 4; ++q)
                                 b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
-                            sm100::tmem_wait_ld();
-                            uint32_t w[4];
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const int bq[4] = {b4[q].x, b4[q].y, b4[q].z, b4[q].w};
-                                uint32_t packed4 = 0;
-#pragma unroll
-                                for (int b = 0; b < 4; ++b) {
-                                    int v = (r[q * 4 + b] + bq[b]) >> ly.shift;
-                                    v = min(max(v, 0), 127);
-                                    packed4 |= static_cast<uint32_t>(v) << (8 * b);
-                                }
-                                w[q] = packed4;
+                        };
+                        int32_t ra[16], rb[16];
+                        int4 ba[4], bb[4];
+                        sm100::tmem_ld16(t_row + c_beg, ra);
+                        load_bias(ba, c_beg);
+                        sm100::tmem_wait_ld();
+                        for (int c0 = c_beg; c0 < c_end; c0 += 32) {
+                            const bool has_b = c0 + 16 < c_end;
+                            if (has_b) {
+                                sm100::tmem_ld16(t_row + c0 + 16, rb);
+                                load_bias(bb, c0 + 16);
                             }
-                            sm100::st_shared_v4(out + (c0 >> 4) * 2048u + row * 16u, w[0], w[1], w[2], w[3]);
+                            requant(ra, ba, c0);
+                            sm100::tmem_wait_ld();
+                            if (!has_b)
+                                break;
+                            if (c0 + 32 < c_end) {
+                                sm100::tmem_ld16(t_row + c0 + 32, ra);
+                                load_bias(ba, c0 + 32);
+                            }
+                            requant(rb, bb, c0 + 16);
+                            sm100::tmem_wait_ld();
                         }
                         sm100::tc_fence_before();
                         sm100::fence_proxy_async_smem();

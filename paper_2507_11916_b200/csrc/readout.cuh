@@ -22,6 +22,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace bida_gpu {
 
@@ -113,6 +114,94 @@ __device__ __forceinline__ int warp_quantile_exact(double (&lg)[CS], int C, doub
         return 0;
     }
     return hit >= 0 ? hit : C - 1;
+}
+
+} // namespace bida_gpu
+
+namespace bida_gpu {
+
+// Warp-parallel certified readout for one (state, member): same decision
+// rule and error bound as certified_readout.cuh (thread-per-state), with the
+// classes spread over lanes.  Logits lg are exact float64; d_c = lg_c - max
+// is formed in float64 and rounded once to float32, exp is ex2.approx, and
+// the tail sums T_k = sum_{c>k} e_c and Z come from warp scans.  Terms with
+// d_c < -88 underflow (< 1e-38 absolute, far below the comparison slack) and
+// are excluded from the relative bound.  Undecided -> exact sequential replay.
+template <int CS>
+__device__ __forceinline__ int warp_quantile_certified(double (&lg)[CS], int C, double thr, float uLo,
+                                                       float uHi, double *scratch, int lane, int *err_bits) {
+    bool finite = true;
+    double mx = -INFINITY;
+#pragma unroll
+    for (int s = 0; s < CS; ++s)
+        if (lane + 32 * s < C) {
+            finite &= isfinite(lg[s]);
+            mx = fmax(mx, lg[s]);
+        }
+    if (__all_sync(kFull, finite)) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+        constexpr float kLog2e = 1.4426950408889634f;
+        float e[CS];
+        float dmax = 0.0f;
+        float slot_sum[CS];
+#pragma unroll
+        for (int s = 0; s < CS; ++s) {
+            e[s] = 0.0f;
+            if (lane + 32 * s < C) {
+                const float d = static_cast<float>(lg[s] - mx);
+                if (d >= -88.0f)
+                    dmax = fmaxf(dmax, -d);
+                e[s] = sm100::ex2_approx(d * kLog2e);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            dmax = fmaxf(dmax, __shfl_xor_sync(kFull, dmax, o));
+        // inclusive suffix sums within each slot: S_incl(lane) = sum_{l' >= lane} e
+        float incl[CS];
+#pragma unroll
+        for (int s = 0; s < CS; ++s) {
+            float v = e[s];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float t = __shfl_down_sync(kFull, v, o);
+                if (lane + o < 32)
+                    v += t;
+            }
+            incl[s] = v;
+            slot_sum[s] = __shfl_sync(kFull, v, 0);
+        }
+        float Z = 0.0f;
+#pragma unroll
+        for (int s = 0; s < CS; ++s)
+            Z += slot_sum[s];
+        const float eta = 1.0e-6f * (dmax + 1.0f);
+        const float rho = 2.2f * (eta + static_cast<float>(C + 4) * 5.9604645e-8f);
+        const float A = uLo * Z * (1.0f - 2.1f * rho);
+        const float B = uHi * Z * (1.0f + 2.1f * rho);
+        int above = 0;       // classes k with T_k > A
+        bool ambiguous = false;
+        float later = 0.0f;  // sum of slots after s
+#pragma unroll
+        for (int s = CS - 1; s >= 0; --s) {
+            const int c = lane + 32 * s;
+            // exclusive suffix = next lane's inclusive suffix (no cancellation)
+            float excl = __shfl_down_sync(kFull, incl[s], 1);
+            if (lane == 31)
+                excl = 0.0f;
+            const float Tk = later + excl;  // sum_{c' > c}
+            const bool live = c < C;
+            const bool over = live && Tk > A;
+            above += __popc(__ballot_sync(kFull, over));
+            ambiguous |= __any_sync(kFull, over && !(Tk > B));
+            later += slot_sum[s];
+        }
+        if (!ambiguous)
+            return above;  // smallest k with T_k <= A (T_k non-increasing in k)
+    }
+    return warp_quantile_exact<CS>(lg, C, thr, scratch, lane, err_bits);
 }
 
 } // namespace bida_gpu

@@ -87,11 +87,11 @@ __device__ __forceinline__ uint64_t make_smem_desc(uint32_t saddr, uint32_t lbo,
     return d;  // base_offset 0, lbo_mode 0, layout_type 0 (SWIZZLE_NONE)
 }
 
-// Instruction descriptor for kind::i8: D s32, A s8, B s8, both K-major,
+// Instruction descriptor for kind::i8: D s32, A u8, B s8, both K-major,
 // M = 128, N = n (multiple of 16, <= 256).
 __device__ __forceinline__ uint32_t make_idesc_i8(uint32_t n) {
     return (2u << 4)            // c_format = S32
-           | (1u << 7)          // a_format = signed int8
+           | (0u << 7)          // a_format = unsigned int8 (activations 0..255)
            | (1u << 10)         // b_format = signed int8
            | ((n >> 3) << 17)   // N >> 3
            | ((128u >> 4) << 24);  // M >> 4
@@ -132,6 +132,14 @@ __device__ __forceinline__ void st_shared_v4(uint32_t saddr, uint32_t a, uint32_
 }
 __device__ __forceinline__ void st_shared_u8(uint32_t saddr, uint32_t v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+
+// Saturating pack of four int32 to u8 (0..255): bytes [a, b, c, d].
+__device__ __forceinline__ uint32_t pack_sat_u8x4(int a, int b, int c, int d) {
+    uint32_t hi, out;
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(d), "r"(c));
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(out) : "r"(b), "r"(a), "r"(hi));
+    return out;
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {

@@ -3,7 +3,7 @@
 The reference has no MLP; BMLP1 extends its BLIN1 linear
 ensemble (batch_eval.hpp:107-131) to hidden layers while keeping the same
 readout (softmax -> quantile_class -> ensemble_min).  Weights and activations
-are integers so that tensor-core int8 MMA with int32 accumulation computes the
+are integers (u8 activations, s8 weights) so that tensor-core 8-bit MMA with int32 accumulation computes the
 logits exactly in any summation order — h is bit-exact by construction.
 
 File layout (little-endian):
@@ -13,7 +13,7 @@ File layout (little-endian):
         i32 bias[out]
         u32 shift       (hidden layers only)
     per member: f32 out_scale
-    hidden: a' = clamp((bias + W a) >> shift, 0, 127); output: logit = (bias + W a) * out_scale
+    hidden: a' = clamp((bias + W a) >> shift, 0, 255); output: logit = (bias + W a) * out_scale
 """
 from __future__ import annotations
 
@@ -86,7 +86,7 @@ def forward_int(layers, x: np.ndarray) -> np.ndarray:
     for li, ly in enumerate(layers):
         acc = a @ ly.W.astype(np.int64).T + ly.bias.astype(np.int64)
         if li < len(layers) - 1:
-            a = np.clip(acc >> ly.shift, 0, 127)
+            a = np.clip(acc >> ly.shift, 0, 255)
         else:
             return acc
     return a
@@ -120,7 +120,7 @@ def _one_hot(domain: int, packed: np.ndarray) -> np.ndarray:
 def make_bmlp1(domain, hidden=(512, 512), classes: int = 21, ensemble: int = 1, seed: int = 0,
                logit_std: float = 2.5) -> bytes:
     """Seeded random BMLP1 model with calibrated shifts (activations use the
-    0..127 range) and an output scale giving logits of std ~logit_std."""
+    0..255 range) and an output scale giving logits of std ~logit_std."""
     d = domain_id(domain)
     F = FEATURES[d]
     rng = np.random.default_rng(seed)
@@ -136,9 +136,9 @@ def make_bmlp1(domain, hidden=(512, 512), classes: int = 21, ensemble: int = 1, 
             acc = a @ W.astype(np.int64).T + b
             if li < len(dims) - 2:
                 p = np.percentile(np.abs(acc), 95)
-                shift = int(max(0, np.ceil(np.log2(max(p, 1) / 100.0))))
+                shift = int(max(0, np.ceil(np.log2(max(p, 1) / 200.0))))
                 layers.append(Layer(W, b, shift))
-                a = np.clip(acc >> shift, 0, 127)
+                a = np.clip(acc >> shift, 0, 255)
             else:
                 layers.append(Layer(W, b, 0))
                 sd = float(acc.std()) or 1.0

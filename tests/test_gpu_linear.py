@@ -184,3 +184,25 @@ def test_concurrent_callers_share_a_handle(orc):
         [t.start() for t in th]
         [t.join() for t in th]
     assert not errors
+
+
+@pytest.mark.parametrize("q", [0.25, 0.5, 0.75, 1.0, 0.3])
+def test_exact_ties_take_exact_replay(orc, q):
+    """Zero weights: uniform softmax, cum_k = (k+1)/C lands exactly on q -
+    the certified float32 readout must defer to the float64 replay."""
+    W = np.zeros((1, 4, 480), np.float32)
+    packed = bida.random_walks("rc", 200, 0, 20, seed=3)
+    with bida.LinearModelBackend("rc", W, 4, q) as be:
+        h = be.evaluate(packed)
+    assert (h == orc.linear_evaluate(RC, W, q, packed)).all()
+
+
+@pytest.mark.parametrize("scale,C", [(50.0, 21), (1e-6, 21), (5.0, 200)])
+def test_extreme_logit_scales(orc, scale, C):
+    rng = np.random.default_rng(int(scale * 7) + C)
+    W = rng.uniform(-scale, scale, (2, C, 480)).astype(np.float32)
+    packed = bida.random_walks("rc", 1500, 0, 30, seed=C)
+    for q in (0.5, 0.999, 1.0, 0.001):
+        with bida.LinearModelBackend("rc", W, C, q) as be:
+            h = be.evaluate(packed)
+        assert (h == orc.linear_evaluate(RC, W, q, packed)).all(), q
