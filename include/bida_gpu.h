@@ -117,6 +117,11 @@ int bida_gpu_evaluate_device(bida_gpu_evaluator *ev, const void *d_packed, int64
 int bida_gpu_stream_status(bida_gpu_evaluator *ev);
 
 int bida_gpu_info(const bida_gpu_evaluator *ev, bida_gpu_model_info *out);
+/* Diagnostics (MLP handles): record a clock64 timeline of CTA 0's warps into
+ * the DEVICE buffer `dev_buf` (int64 [warps][bida_gpu_trace_slots()]) on every
+ * subsequent launch; NULL switches it off. */
+int bida_gpu_debug_trace(bida_gpu_evaluator *ev, long long *dev_buf);
+int bida_gpu_trace_slots(void);
 /* Number of kernel launches issued by this handle so far (bench evidence). */
 int64_t bida_gpu_launch_count(const bida_gpu_evaluator *ev);
 int bida_gpu_destroy(bida_gpu_evaluator *ev);

@@ -54,6 +54,8 @@ EXPORTS = [
     "bida_gpu_evaluate_device",
     "bida_gpu_stream_status",
     "bida_gpu_info",
+    "bida_gpu_debug_trace",
+    "bida_gpu_trace_slots",
     "bida_gpu_launch_count",
     "bida_gpu_destroy",
 ]
@@ -89,6 +91,7 @@ def lib() -> C.CDLL:
     L.bida_gpu_evaluate_device.argtypes = [H, vp, i64, vp, vp, vp]
     L.bida_gpu_stream_status.argtypes = [H]
     L.bida_gpu_info.argtypes = [H, C.POINTER(ModelInfo)]
+    L.bida_gpu_debug_trace.argtypes = [H, vp]
     L.bida_gpu_launch_count.argtypes = [H]
     L.bida_gpu_launch_count.restype = i64
     L.bida_gpu_destroy.argtypes = [H]

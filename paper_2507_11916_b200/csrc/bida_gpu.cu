@@ -592,6 +592,15 @@ int bida_gpu_info(const bida_gpu_evaluator *ev, bida_gpu_model_info *out) {
     return BIDA_OK;
 }
 
+int bida_gpu_debug_trace(bida_gpu_evaluator *ev, long long *dev_buf) {
+    if (!ev || ev->kind != BIDA_MODEL_MLP)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "debug trace needs an MLP evaluator");
+    mlp_set_trace(ev->mlp, dev_buf);
+    return BIDA_OK;
+}
+
+int bida_gpu_trace_slots(void) { return mlp_trace_slots(); }
+
 int64_t bida_gpu_launch_count(const bida_gpu_evaluator *ev) {
     return ev ? ev->launches.load(std::memory_order_relaxed) : 0;
 }

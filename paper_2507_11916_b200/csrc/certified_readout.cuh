@@ -71,45 +71,45 @@ template <int CM>
 __device__ __forceinline__ int readout_certified(const int32_t (&v)[CM], int C, float sf, double sd,
                                                  const ReadoutConsts &k, bool *bad, bool *fell_back) {
     constexpr float kLog2e = 1.4426950408889634f;
+    // pass 1: logits in float32, their max and max magnitude
+    float e[CM];
     float m = -INFINITY, lam = 0.0f;
 #pragma unroll
     for (int c = 0; c < CM; ++c) {
+        e[c] = static_cast<float>(v[c]) * sf;
         if (c < C) {
-            const float l = static_cast<float>(v[c]) * sf;
-            m = fmaxf(m, l);
-            lam = fmaxf(lam, fabsf(l));
+            m = fmaxf(m, e[c]);
+            lam = fmaxf(lam, fabsf(e[c]));
         }
     }
     const float eta = 1.0e-6f * (lam + 1.0f);
     const float rho = 2.2f * (eta + static_cast<float>(C + 4) * 5.9604645e-8f);
     *fell_back = false;
     if (rho < 1.0e-2f) {  // false for NaN / inf / huge logits
-        // e_c = exp(l_c - m), recomputed identically in both passes
-        auto ec = [&](int c) { return sm100::ex2_approx((static_cast<float>(v[c]) * sf - m) * kLog2e); };
+        // pass 2: e_c = exp(l_c - m) (independent, pipelined), Z
         float Z = 0.0f;
 #pragma unroll
-        for (int c = 0; c < CM; ++c)
-            if (c < C)
-                Z += ec(c);
+        for (int c = 0; c < CM; ++c) {
+            e[c] = c < C ? sm100::ex2_approx((e[c] - m) * kLog2e) : 0.0f;
+            Z += e[c];
+        }
         const float A = k.uLo * Z * (1.0f - 2.1f * rho);
         const float B = k.uHi * Z * (1.0f + 2.1f * rho);
-        float T = 0.0f;  // T_k = sum_{c > k} e_c
-        int ans = 0;
-        bool certified = true, done = false;
+        // pass 3, branch-free: T_k = sum_{c > k} e_c; the answer is the number
+        // of classes with T_k > A (T is non-increasing in k); every such class
+        // must also satisfy T_k > B, else the float32 bound cannot decide.
+        float T = 0.0f;
+        int above = 0;
+        bool ambiguous = false;
 #pragma unroll
         for (int c = CM - 1; c >= 0; --c) {
-            if (c < C && !done) {
-                if (T > A) {
-                    ans = c + 1;
-                    certified = T > B;
-                    done = true;
-                } else {
-                    T += ec(c);
-                }
-            }
+            const bool over = c < C && T > A;
+            above += over ? 1 : 0;
+            ambiguous |= over && !(T > B);
+            T += e[c];
         }
-        if (certified)
-            return ans;
+        if (!ambiguous)
+            return above;
     }
     *fell_back = true;
     int32_t spill[CM];  // only this branch touches local memory

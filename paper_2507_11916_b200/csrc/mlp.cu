@@ -43,6 +43,7 @@ constexpr int kMaxStages = 6;
 constexpr int kStageBytes = 16384;
 constexpr int kMlpThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2-9 two epilogue groups
 constexpr int kKChunk = 32;       // bytes of K per MMA instruction
+enum MlpMode { kPair = 0, kSplit = 1, kResident = 2 };
 
 struct MlpLayer {
     int K, N;          // padded input width (multiple of 32), output width (multiple of 16)
@@ -60,8 +61,9 @@ struct MlpParams {
     double scale_d[kMaxMembers];
     ReadoutConsts rk;
     uint32_t tmem_cols;
-    int slots;          // 2: two tiles in flight (ping-pong); 1: both groups split one tile's columns
-    int stages;         // weight ring depth (16 KB stages)
+    int mode;           // MlpMode
+    int stages;         // weight ring depth (16 KB stages), streaming modes
+    int wbytes, wbytes_pad;  // weight image bytes (resident mode)
     int xbytes, ybytes; // activation buffers per slot (even / odd layer inputs)
     // batch
     const void *packed;
@@ -69,7 +71,10 @@ struct MlpParams {
     int32_t *h_out;
     double *logits_out;
     int *err;
+    long long *trace;   // optional debug timeline (CTA 0): [warp][kTraceSlots] (clock64, tag)
 };
+
+constexpr int kTraceSlots = 256;
 
 struct MlpModel {
     MlpParams p;
@@ -78,7 +83,11 @@ struct MlpModel {
     size_t smem = 0;
     int grid_cap = 148;
     int cm = 32;
+    long long *trace = nullptr;  // debug timeline buffer (bida_gpu_debug_trace)
 };
+
+void mlp_set_trace(MlpModel *m, long long *dev_buf) { m->trace = dev_buf; }
+int mlp_trace_slots() { return kTraceSlots; }
 
 namespace {
 thread_local std::string g_err;
@@ -90,30 +99,52 @@ __device__ __forceinline__ int chunks_per_stage(int N) {
     const int c = kStageBytes / (N * kKChunk);
     return c < 1 ? 1 : c;
 }
+
+// Debug timeline: lane 0 of each warp of CTA 0 appends (clock64 << 8 | tag).
+struct Tracer {
+    long long *buf = nullptr;
+    int n = 0;
+    __device__ void operator()(int tag) {
+        if (buf && n < kTraceSlots)
+            buf[n++] = (clock64() << 8) | (tag & 0xFF);
+    }
+};
 } // namespace
 
-// One CTA per SM, persistent over the CTA's tiles of 128 states.  Local tile
-// k of this CTA is t = blockIdx.x + k * gridDim.x; with two slots, tiles
-// alternate between slot 0 and 1 (epilogue group g owns slot g), and the MMA
-// issuer interleaves the slots layer by layer so one slot's tensor-core work
-// overlaps the other slot's epilogue.
+// One CTA per SM, persistent over the CTA's tiles of 128 states (local tile k
+// of this CTA is t = blockIdx.x + k * gridDim.x).  A "job" is one (tile,
+// ensemble member) pair.  Three schedules (MlpMode):
+//   kPair     : two jobs in flight, epilogue group g owns every other tile
+//               (TMEM columns [256g, 256g+256)); the MMA issuer interleaves
+//               the two tiles layer by layer; weights streamed per tile.
+//   kSplit    : one job in flight, the two groups split every hidden layer's
+//               columns; weights streamed (wide models, N > 256).
+//   kResident : the whole weight image is loaded into SMEM once per CTA;
+//               groups split hidden columns; group 1 encodes job j+1 while
+//               group 0 reads out job j, and TMEM is double-buffered by job
+//               parity so job j+1's MMAs overlap job j's readout.
 template <int DOMAIN, int CM>
 __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_constant__ MlpParams p) {
     using T = DomainTraits<DOMAIN>;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int slot_bytes = p.xbytes + p.ybytes;
-    uint8_t *stages = smem + p.slots * slot_bytes;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(stages + p.stages * kStageBytes);
+    const int mode = p.mode;
+    const int nsets = mode == kPair ? 2 : 1;  // activation buffer sets
+    const int set_bytes = p.xbytes + p.ybytes;
+    uint8_t *wbuf = smem + nsets * set_bytes;  // ring stages or resident image
+    const int wbuf_bytes = mode == kResident ? p.wbytes_pad : p.stages * kStageBytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(wbuf + wbuf_bytes);
     uint64_t *full = bars;                       // [kMaxStages]
     uint64_t *empty = bars + kMaxStages;         // [kMaxStages]
     uint64_t *act_ready = bars + 2 * kMaxStages; // [2]
     uint64_t *d_full = act_ready + 2;            // [2]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(d_full + 2);
+    uint64_t *x_ready = d_full + 2;              // resident: one-hot of the next job written
+    uint64_t *w_ready = x_ready + 1;             // resident: weight image landed
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w_ready + 1);
 
     const int warp = threadIdx.x >> 5;
     const long long ntiles = (p.n + kTileM - 1) / kTileM;
     const long long nloc = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const int slots = p.slots;
+    const bool tdbl = p.tmem_cols == 512u;  // TMEM halves available for double-buffering
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kMaxStages; ++s) {
@@ -121,9 +152,11 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             sm100::mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
-            sm100::mbar_init(&act_ready[s], slots == 2 ? 128 : 256);
+            sm100::mbar_init(&act_ready[s], mode == kPair ? 128 : 256);
             sm100::mbar_init(&d_full[s], 1);
         }
+        sm100::mbar_init(x_ready, 128);
+        sm100::mbar_init(w_ready, 1);
         sm100::fence_barrier_init();
     }
     if (warp == 1)
@@ -132,59 +165,91 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
     __syncthreads();
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    Tracer tr;
+    if (p.trace && blockIdx.x == 0 && lane_id() == 0)
+        tr.buf = p.trace + static_cast<long long>(warp) * kTraceSlots;
 
     if (warp == 0) {
         // ------------------------------------------------ weight producer
-        if (lane_id() == 0) {
-            int s = 0;
-            uint32_t ph = 0;
-            for (long long k0 = 0; k0 < nloc; k0 += slots)
-                for (int e = 0; e < p.E; ++e)
-                    for (int l = 0; l < p.nl; ++l)
-                        for (int sl = 0; sl < slots && k0 + sl < nloc; ++sl) {
-                            const MlpLayer &ly = p.layer[e][l];
-                            const int nch = ly.K / kKChunk, cps = chunks_per_stage(ly.N);
-                            const uint32_t cbytes = static_cast<uint32_t>(ly.N) * kKChunk;
-                            for (int kc = 0; kc < nch; kc += cps) {
-                                const int cnt = min(cps, nch - kc);
-                                sm100::mbar_wait(&empty[s], ph ^ 1u);
-                                sm100::mbar_arrive_expect_tx(&full[s], cnt * cbytes);
-                                sm100::bulk_g2s(stages + s * kStageBytes, p.wimg + ly.woff + static_cast<size_t>(kc) * cbytes,
-                                                cnt * cbytes, &full[s]);
-                                if (++s == p.stages) {
-                                    s = 0;
-                                    ph ^= 1u;
+        if (lane_id() == 0 && nloc > 0) {
+            if (mode == kResident) {
+                sm100::mbar_arrive_expect_tx(w_ready, static_cast<uint32_t>(p.wbytes));
+                for (int off = 0; off < p.wbytes; off += kStageBytes) {
+                    const int b = min(kStageBytes, p.wbytes - off);
+                    sm100::bulk_g2s(wbuf + off, p.wimg + off, static_cast<uint32_t>(b), w_ready);
+                }
+            } else {
+                const int per = mode == kPair ? 2 : 1;
+                int s = 0;
+                uint32_t ph = 0;
+                for (long long k0 = 0; k0 < nloc; k0 += per)
+                    for (int e = 0; e < p.E; ++e)
+                        for (int l = 0; l < p.nl; ++l)
+                            for (int sl = 0; sl < per && k0 + sl < nloc; ++sl) {
+                                const MlpLayer &ly = p.layer[e][l];
+                                const int nch = ly.K / kKChunk, cps = chunks_per_stage(ly.N);
+                                const uint32_t cbytes = static_cast<uint32_t>(ly.N) * kKChunk;
+                                for (int kc = 0; kc < nch; kc += cps) {
+                                    const int cnt = min(cps, nch - kc);
+                                    sm100::mbar_wait(&empty[s], ph ^ 1u);
+                                    sm100::mbar_arrive_expect_tx(&full[s], cnt * cbytes);
+                                    sm100::bulk_g2s(wbuf + s * kStageBytes,
+                                                    p.wimg + ly.woff + static_cast<size_t>(kc) * cbytes, cnt * cbytes,
+                                                    &full[s]);
+                                    if (++s == p.stages) {
+                                        s = 0;
+                                        ph ^= 1u;
+                                    }
                                 }
                             }
-                        }
+            }
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
-        if (lane_id() == 0) {
+        if (lane_id() == 0 && nloc > 0) {
             int s = 0;
-            uint32_t ph = 0, aph[2] = {0u, 0u};
-            const uint32_t sbase = sm100::smem_u32(smem), sS = sm100::smem_u32(stages);
-            for (long long k0 = 0; k0 < nloc; k0 += slots)
-                for (int e = 0; e < p.E; ++e)
+            uint32_t ph = 0, aph[2] = {0u, 0u}, xph = 0;
+            const uint32_t sbase = sm100::smem_u32(smem), sW = sm100::smem_u32(wbuf);
+            if (mode == kResident)
+                sm100::mbar_wait(w_ready, 0);
+            const int per = mode == kPair ? 2 : 1;
+            long long job = 0;
+            for (long long k0 = 0; k0 < nloc; k0 += per)
+                for (int e = 0; e < p.E; ++e, ++job)
                     for (int l = 0; l < p.nl; ++l)
-                        for (int sl = 0; sl < slots && k0 + sl < nloc; ++sl) {
+                        for (int sl = 0; sl < per && k0 + sl < nloc; ++sl) {
                             const MlpLayer &ly = p.layer[e][l];
-                            sm100::mbar_wait(&act_ready[sl], aph[sl]);
-                            aph[sl] ^= 1u;
+                            tr(10 + l + 4 * sl);
+                            if (mode == kResident && l == 0) {
+                                sm100::mbar_wait(x_ready, xph);
+                                xph ^= 1u;
+                            } else {
+                                sm100::mbar_wait(&act_ready[sl], aph[sl]);
+                                aph[sl] ^= 1u;
+                            }
+                            tr(20 + l + 4 * sl);
                             sm100::tc_fence_after();
-                            const uint32_t abase = sbase + sl * slot_bytes + ((l & 1) ? p.xbytes : 0);
-                            const uint32_t dcol = tmem + sl * 256u;
+                            const uint32_t abase = sbase + sl * set_bytes + ((l & 1) ? p.xbytes : 0);
+                            const uint32_t dcol =
+                                tmem + (mode == kPair ? sl * 256u : (mode == kResident && tdbl ? (job & 1) * 256u : 0u));
                             const uint32_t lbo_b = static_cast<uint32_t>(ly.N) * 16u;
-                            const int nch = ly.K / kKChunk, cps = chunks_per_stage(ly.N);
+                            const int nch = ly.K / kKChunk;
+                            const int cps = mode == kResident ? nch : chunks_per_stage(ly.N);
+                            const uint32_t cbytes = static_cast<uint32_t>(ly.N) * kKChunk;
                             const uint32_t idesc_full = sm100::make_idesc_i8(ly.N < 256 ? ly.N : 256);
                             for (int kc = 0; kc < nch; kc += cps) {
                                 const int cnt = min(cps, nch - kc);
-                                sm100::mbar_wait(&full[s], ph);
-                                sm100::tc_fence_after();
-                                const uint32_t stg = sS + s * kStageBytes;
+                                uint32_t stg;
+                                if (mode == kResident) {
+                                    stg = sW + static_cast<uint32_t>(ly.woff) + kc * cbytes;
+                                } else {
+                                    sm100::mbar_wait(&full[s], ph);
+                                    sm100::tc_fence_after();
+                                    stg = sW + s * kStageBytes;
+                                }
                                 for (int j = 0; j < cnt; ++j) {
                                     const uint64_t adesc = sm100::make_smem_desc(abase + (kc + j) * 4096u, 2048u, 128u);
-                                    const uint32_t cb = stg + j * static_cast<uint32_t>(ly.N) * kKChunk;
+                                    const uint32_t cb = stg + j * cbytes;
                                     for (int n0 = 0; n0 < ly.N; n0 += 256) {
                                         const int nn = ly.N - n0 < 256 ? ly.N - n0 : 256;
                                         const uint64_t bdesc = sm100::make_smem_desc(cb + (n0 / 8) * 128u, lbo_b, 128u);
@@ -193,13 +258,16 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                                       (kc + j) > 0 ? 1u : 0u);
                                     }
                                 }
-                                sm100::mma_commit(&empty[s]);
-                                if (++s == p.stages) {
-                                    s = 0;
-                                    ph ^= 1u;
+                                if (mode != kResident) {
+                                    sm100::mma_commit(&empty[s]);
+                                    if (++s == p.stages) {
+                                        s = 0;
+                                        ph ^= 1u;
+                                    }
                                 }
                             }
                             sm100::mma_commit(&d_full[sl]);
+                            tr(30 + l + 4 * sl);
                         }
         }
     } else {
@@ -207,20 +275,23 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
         const int grp = (warp - 2) >> 2;           // epilogue group 0 / 1
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
         const int row = quad * 32 + lane_id();     // tile row == TMEM lane
-        const int sl = slots == 2 ? grp : 0;
-        const bool leader = slots == 2 || grp == 0;  // encodes, reads out, writes h
-        const uint32_t t_row = tmem + sl * 256u + (static_cast<uint32_t>(quad * 32) << 16);
-        const uint32_t sX = sm100::smem_u32(smem) + sl * slot_bytes;
+        const int sl = mode == kPair ? grp : 0;
+        const uint32_t sX = sm100::smem_u32(smem) + sl * set_bytes;
         const uint32_t sY = sX + p.xbytes;
         uint64_t *my_ready = &act_ready[sl];
         uint64_t *my_full = &d_full[sl];
         uint32_t dph = 0;
-        const long long kstep = slots == 2 ? 2 : 1;
-        // packed states are prefetched one tile ahead (HBM latency off the critical path)
+        // pair: this group's own tiles; split/resident: every tile of the CTA
+        const long long kfirst = mode == kPair ? grp : 0, kstep = mode == kPair ? 2 : 1;
+        // who encodes / reads out: pair -> both groups (own tiles); split -> group 0;
+        // resident -> group 1 encodes (one job ahead), group 0 reads out
+        const bool encoder = mode == kPair || (mode == kSplit ? grp == 0 : grp == 1);
+        const bool reader = mode == kPair || grp == 0;
+
         auto load_state = [&](long long kk, uint64_t &lo_, uint64_t &hi_) {
             lo_ = hi_ = 0;
             const long long s_ = (blockIdx.x + kk * gridDim.x) * kTileM + row;
-            if (kk < nloc && s_ < p.n && leader) {
+            if (kk < nloc && s_ < p.n) {
                 if constexpr (T::PB == 16) {
                     const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2 *>(p.packed) + s_);
                     lo_ = v.x;
@@ -230,60 +301,78 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                 }
             }
         };
-        uint64_t nlo, nhi;
-        load_state(slots == 2 ? grp : 0, nlo, nhi);
-        for (long long k = (slots == 2 ? grp : 0); k < nloc; k += kstep) {
-            const long long t = blockIdx.x + k * gridDim.x;
-            const long long st = t * kTileM + row;
+        auto state_bad = [&](uint64_t lo_, uint64_t hi_) {
+            bool b = false;
+#pragma unroll
+            for (int q = 0; q < T::NNZ; ++q) {
+                const int j = position_feature<DOMAIN>(lo_, hi_, q);
+                b |= j < 0 || j >= T::F;
+            }
+            return b;
+        };
+        // one-hot row of a packed state into X (layer 0's A operand), then publish
+        auto encode = [&](uint64_t lo_, uint64_t hi_, bool live_, uint64_t *bar) {
+            tr(40);
+            for (int c16 = 0; c16 < p.Fpad / 16; ++c16)
+                sm100::st_shared_v4(sX + c16 * 2048u + row * 16u, 0u, 0u, 0u, 0u);
+            if (live_) {
+#pragma unroll
+                for (int q = 0; q < T::NNZ; ++q) {
+                    const int j = position_feature<DOMAIN>(lo_, hi_, q);
+                    sm100::st_shared_u8(sX + (j >> 4) * 2048u + row * 16u + (j & 15), 1u);
+                }
+            }
+            sm100::fence_proxy_async_smem();
+            tr(41);
+            sm100::mbar_arrive(bar);
+        };
+        auto tile_valid = [&](long long kk) { return kk < nloc && (blockIdx.x + kk * gridDim.x) * kTileM + row < p.n; };
+
+        uint64_t nlo = 0, nhi = 0;
+        load_state(kfirst, nlo, nhi);
+        if (mode == kResident && encoder && nloc > 0)  // first job's one-hot
+            encode(nlo, nhi, tile_valid(kfirst) && !state_bad(nlo, nhi), x_ready);
+        long long job = kfirst * p.E;
+        for (long long k = kfirst; k < nloc; k += kstep) {
+            const long long st = (blockIdx.x + k * gridDim.x) * kTileM + row;
             const bool valid = st < p.n;
             const uint64_t lo = nlo, hi = nhi;
             load_state(k + kstep, nlo, nhi);
-            int idx[T::NNZ];
-            bool bad = false;
-#pragma unroll
-            for (int q = 0; q < T::NNZ; ++q) {
-                idx[q] = position_feature<DOMAIN>(lo, hi, q);
-                bad |= idx[q] < 0 || idx[q] >= T::F;
-            }
-            bad = bad && valid && leader;
-            if (bad)
+            const bool bad = valid && state_bad(lo, hi);
+            if (bad && reader)
                 raise_error(p.err, kErrState);
             const bool live = valid && !bad;
             int hmin = 0x7fffffff;
             bool dist_bad = false;
-            for (int e = 0; e < p.E; ++e) {
-                if (leader) {
-                    // ---- encode: one-hot row into X (layer 0's A operand)
-                    for (int c16 = 0; c16 < p.Fpad / 16; ++c16)
-                        sm100::st_shared_v4(sX + c16 * 2048u + row * 16u, 0u, 0u, 0u, 0u);
-                    if (live) {
-#pragma unroll
-                        for (int q = 0; q < T::NNZ; ++q) {
-                            const int j = idx[q];
-                            sm100::st_shared_u8(sX + (j >> 4) * 2048u + row * 16u + (j & 15), 1u);
-                        }
-                    }
-                    sm100::fence_proxy_async_smem();
+            for (int e = 0; e < p.E; ++e, ++job) {
+                const uint32_t tcol = mode == kPair ? sl * 256u : (mode == kResident && tdbl ? (job & 1) * 256u : 0u);
+                const uint32_t t_row = tmem + tcol + (static_cast<uint32_t>(quad * 32) << 16);
+                if (mode != kResident) {
+                    if (encoder)
+                        encode(lo, hi, live, my_ready);
+                    else
+                        sm100::mbar_arrive(my_ready);
                 }
-                sm100::mbar_arrive(my_ready);
                 for (int l = 0; l < p.nl; ++l) {
                     const MlpLayer &ly = p.layer[e][l];
+                    tr(50 + l);
                     sm100::mbar_wait(my_full, dph);
+                    tr(60 + l);
                     dph ^= 1u;
                     sm100::tc_fence_after();
                     const int32_t *bias = p.bias + ly.boff;
                     if (l + 1 < p.nl) {
-                        // hidden layer epilogue: bias, shift, clamp -> int8 A operand of layer l+1
+                        // hidden layer epilogue: (acc + bias) >> shift -> u8 A operand of layer l+1
                         const uint32_t out = ((l + 1) & 1) ? sY : sX;
-                        const int half = slots == 2 ? ly.N : ly.N / 2;
-                        const int c_beg = slots == 2 ? 0 : grp * half, c_end = c_beg + half;
+                        const int half = mode == kPair ? ly.N : ly.N / 2;
+                        const int c_beg = mode == kPair ? 0 : grp * half, c_end = c_beg + half;
                         // software-pipelined: the TMEM load of the next 16 columns is in
                         // flight while the current 16 are requantised and stored
                         const int sh = ly.shift;
                         auto requant = [&](const int32_t(&r)[16], const int4(&b4)[4], int c0) {
                             uint32_t w[4];
 #pragma unroll
-                            for (int q = 0; q < 4; ++q)  // (acc + bias) >> shift, saturated to u8 0..255
+                            for (int q = 0; q < 4; ++q)  // saturated to u8 0..255
                                 w[q] = sm100::pack_sat_u8x4((r[q * 4 + 0] + b4[q].x) >> sh, (r[q * 4 + 1] + b4[q].y) >> sh,
                                                             (r[q * 4 + 2] + b4[q].z) >> sh, (r[q * 4 + 3] + b4[q].w) >> sh);
                             sm100::st_shared_v4(out + (c0 >> 4) * 2048u + row * 16u, w[0], w[1], w[2], w[3]);
@@ -317,34 +406,58 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                         }
                         sm100::tc_fence_before();
                         sm100::fence_proxy_async_smem();
+                        tr(70 + l);
                         sm100::mbar_arrive(my_ready);
-                    } else if (leader) {
-                        // output layer: exact integer logits -> certified readout
-                        int32_t v[CM];
+                    } else {
+                        if (reader) {
+                            // output layer: exact integer logits -> certified readout
+                            int32_t v[CM];
 #pragma unroll
-                        for (int c0 = 0; c0 < CM; c0 += 16) {
-                            if (c0 < p.C) {
-                                int32_t r[16];
-                                sm100::tmem_ld16(t_row + c0, r);
-                                sm100::tmem_wait_ld();
+                            for (int c0 = 0; c0 < CM; c0 += 16) {
+                                if (c0 < p.C) {
+                                    int32_t r[16];
+                                    sm100::tmem_ld16(t_row + c0, r);
+                                    int4 b4[4];
 #pragma unroll
-                                for (int j = 0; j < 16; ++j)
-                                    v[c0 + j] = r[j] + ((c0 + j < p.C) ? __ldg(bias + c0 + j) : 0);
+                                    for (int q = 0; q < 4; ++q)
+                                        b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
+                                    sm100::tmem_wait_ld();
+#pragma unroll
+                                    for (int q = 0; q < 4; ++q) {
+                                        v[c0 + 4 * q + 0] = r[4 * q + 0] + b4[q].x;
+                                        v[c0 + 4 * q + 1] = r[4 * q + 1] + b4[q].y;
+                                        v[c0 + 4 * q + 2] = r[4 * q + 2] + b4[q].z;
+                                        v[c0 + 4 * q + 3] = r[4 * q + 3] + b4[q].w;
+                                    }
+                                }
+                            }
+                            sm100::tc_fence_before();
+                            tr(81);
+                            if (p.logits_out && valid) {
+                                double *dst = p.logits_out + (static_cast<size_t>(st) * p.E + e) * p.C;
+                                for (int c = 0; c < p.C; ++c)
+                                    dst[c] = static_cast<double>(v[c]) * p.scale_d[e];
+                            }
+                            bool fb = false;
+                            const int h =
+                                readout_certified<CM>(v, p.C, p.scale_f[e], p.scale_d[e], p.rk, &dist_bad, &fb);
+                            hmin = min(hmin, h);
+                            tr(fb ? 83 : 82);
+                            tr(80);
+                        }
+                        if (mode == kResident && encoder) {
+                            // next job's one-hot: X is free once this job's last layer completed
+                            const bool last_member = e + 1 == p.E;
+                            const long long kn = last_member ? k + 1 : k;
+                            if (kn < nloc) {
+                                const uint64_t elo = last_member ? nlo : lo, ehi = last_member ? nhi : hi;
+                                encode(elo, ehi, tile_valid(kn) && !state_bad(elo, ehi), x_ready);
                             }
                         }
-                        sm100::tc_fence_before();
-                        if (p.logits_out && valid) {
-                            double *dst = p.logits_out + (static_cast<size_t>(st) * p.E + e) * p.C;
-                            for (int c = 0; c < p.C; ++c)
-                                dst[c] = static_cast<double>(v[c]) * p.scale_d[e];
-                        }
-                        bool fb = false;
-                        const int h = readout_certified<CM>(v, p.C, p.scale_f[e], p.scale_d[e], p.rk, &dist_bad, &fb);
-                        hmin = min(hmin, h);
                     }
                 }
             }
-            if (leader && valid) {
+            if (reader && valid) {
                 if (dist_bad)
                     raise_error(p.err, kErrDistribution);
                 p.h_out[st] = (live && !dist_bad) ? hmin : 0;
@@ -522,34 +635,46 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     p.rk.uHi = std::nextafter(static_cast<float>(u + eps64), INFINITY);
     p.xbytes = kTileM * KX;
     p.ybytes = kTileM * KY;
-    const size_t bar_bytes = 8 * (2 * kMaxStages + 4) + 16;
+    p.wbytes = static_cast<int>(img.size());
+    p.wbytes_pad = (p.wbytes + 1023) & ~1023;
+    const size_t bar_bytes = 8 * (2 * kMaxStages + 6) + 16;
     const size_t budget = 227 * 1024;
-    auto stages_for = [&](int slots) -> int {
-        const size_t act = static_cast<size_t>(slots) * (p.xbytes + p.ybytes);
+    const size_t set1 = static_cast<size_t>(p.xbytes) + p.ybytes;
+    auto stages_for = [&](size_t act) -> int {
         if (act + bar_bytes + 2 * kStageBytes > budget)
             return 0;
-        return static_cast<int>(std::min<size_t>(4, (budget - act - bar_bytes) / kStageBytes));
+        return static_cast<int>(std::min<size_t>(kMaxStages, (budget - act - bar_bytes) / kStageBytes));
     };
-    // Two tiles in flight when both accumulators fit TMEM (2 x 256 columns)
-    // and both slots' activation buffers fit shared memory; else one tile
-    // whose columns the two epilogue groups split.
-    if (Nmax <= 256 && stages_for(2) >= 2) {
-        p.slots = 2;
-        p.stages = stages_for(2);
+    auto pow2cols = [](int n) {
+        uint32_t c = 32;
+        while (c < static_cast<uint32_t>(n))
+            c <<= 1;
+        return c;
+    };
+    // 1) every layer <= 256 wide and the whole weight image fits next to one
+    //    activation set: resident
+    // 2) every layer <= 256 wide and two activation sets fit: pair (streamed)
+    // 3) otherwise: split (streamed)
+    if (Nmax <= 256 && set1 + p.wbytes_pad + bar_bytes <= budget) {  // (TMEM double-buffered by job)
+        p.mode = kResident;
+        p.stages = 0;
+        p.tmem_cols = 512u;
+        m->smem = set1 + p.wbytes_pad + bar_bytes;
+    } else if (Nmax <= 256 && stages_for(2 * set1) >= 2) {
+        p.mode = kPair;
+        p.stages = stages_for(2 * set1);
         p.tmem_cols = 512;
-    } else if (stages_for(1) >= 2) {
-        p.slots = 1;
-        p.stages = stages_for(1);
-        uint32_t cols = 32;
-        while (cols < static_cast<uint32_t>(Nmax))
-            cols <<= 1;
-        p.tmem_cols = cols;
+        m->smem = 2 * set1 + static_cast<size_t>(p.stages) * kStageBytes + bar_bytes;
+    } else if (stages_for(set1) >= 2) {
+        p.mode = kSplit;
+        p.stages = stages_for(set1);
+        p.tmem_cols = pow2cols(Nmax);
+        m->smem = set1 + static_cast<size_t>(p.stages) * kStageBytes + bar_bytes;
     } else {
         delete m;
         return fail(err, 1, "BMLP1: model too wide for shared memory");
     }
     m->cm = C <= 32 ? 32 : (C <= 64 ? 64 : 256);
-    m->smem = static_cast<size_t>(p.slots) * (p.xbytes + p.ybytes) + static_cast<size_t>(p.stages) * kStageBytes + bar_bytes;
     m->grid_cap = num_sms;
     cudaError_t ce = cudaMalloc(&m->d_wimg, img.size());
     if (ce == cudaSuccess)
@@ -577,6 +702,7 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
 int mlp_launch(MlpModel *m, int domain, const void *d_packed, int64_t n, int32_t *d_h, double *d_logits,
                int *err_dev, cudaStream_t st, std::atomic<int64_t> *launches) {
     MlpParams p = m->p;  // per-call copy: concurrent launches on one handle are safe
+    p.trace = m->trace;
     p.packed = d_packed;
     p.n = n;
     p.h_out = d_h;
