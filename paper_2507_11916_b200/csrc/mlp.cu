@@ -47,6 +47,7 @@ enum MlpMode { kPair = 0, kSplit = 1, kResident = 2 };
 
 struct MlpLayer {
     int K, N;          // padded input width (multiple of 32), output width (multiple of 16)
+    int cps;           // K-chunks per 16 KB stage (streaming modes)
     int shift;         // hidden layers
     int boff;          // bias offset (int32 elements, multiple of 4)
     long long woff;    // weight image offset (bytes)
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                         for (int l = 0; l < p.nl; ++l)
                             for (int sl = 0; sl < per && k0 + sl < nloc; ++sl) {
                                 const MlpLayer &ly = p.layer[e][l];
-                                const int nch = ly.K / kKChunk, cps = chunks_per_stage(ly.N);
+                                const int nch = ly.K / kKChunk, cps = ly.cps;
                                 const uint32_t cbytes = static_cast<uint32_t>(ly.N) * kKChunk;
                                 for (int kc = 0; kc < nch; kc += cps) {
                                     const int cnt = min(cps, nch - kc);
@@ -206,7 +207,9 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
-        if (lane_id() == 0 && nloc > 0) {
+        // The whole warp walks the schedule (uniform control flow, descriptors
+        // in uniform registers); one elected lane issues the tcgen05 ops.
+        if (nloc > 0) {
             int s = 0;
             uint32_t ph = 0, aph[2] = {0u, 0u}, xph = 0;
             const uint32_t sbase = sm100::smem_u32(smem), sW = sm100::smem_u32(wbuf);
@@ -216,10 +219,16 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             long long job = 0;
             for (long long k0 = 0; k0 < nloc; k0 += per)
                 for (int e = 0; e < p.E; ++e, ++job)
-                    for (int l = 0; l < p.nl; ++l)
+                    for (int l = 0; l < p.nl; ++l) {
+                        const MlpLayer ly = p.layer[e][l];  // one copy per layer, not per MMA
+                        const int nch = ly.K / kKChunk;
+                        const int cps = mode == kResident ? nch : ly.cps;
+                        const uint32_t cbytes = static_cast<uint32_t>(ly.N) * kKChunk;
+                        const uint32_t idesc_a = sm100::make_idesc_i8(ly.N < 256 ? ly.N : 256);
+                        const uint32_t idesc_b = sm100::make_idesc_i8(ly.N > 256 ? ly.N - 256 : 16);
                         for (int sl = 0; sl < per && k0 + sl < nloc; ++sl) {
-                            const MlpLayer &ly = p.layer[e][l];
-                            tr(10 + l + 4 * sl);
+                            if (lane_id() == 0)
+                                tr(10 + l + 4 * sl);
                             if (mode == kResident && l == 0) {
                                 sm100::mbar_wait(x_ready, xph);
                                 xph ^= 1u;
@@ -227,16 +236,14 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                 sm100::mbar_wait(&act_ready[sl], aph[sl]);
                                 aph[sl] ^= 1u;
                             }
-                            tr(20 + l + 4 * sl);
+                            if (lane_id() == 0)
+                                tr(20 + l + 4 * sl);
                             sm100::tc_fence_after();
                             const uint32_t abase = sbase + sl * set_bytes + ((l & 1) ? p.xbytes : 0);
                             const uint32_t dcol =
                                 tmem + (mode == kPair ? sl * 256u : (mode == kResident && tdbl ? (job & 1) * 256u : 0u));
-                            const uint32_t lbo_b = static_cast<uint32_t>(ly.N) * 16u;
-                            const int nch = ly.K / kKChunk;
-                            const int cps = mode == kResident ? nch : chunks_per_stage(ly.N);
-                            const uint32_t cbytes = static_cast<uint32_t>(ly.N) * kKChunk;
-                            const uint32_t idesc_full = sm100::make_idesc_i8(ly.N < 256 ? ly.N : 256);
+                            // descriptor of k-step 0; k-step i adds i*4096 B (A) / i*cbytes (B)
+                            uint64_t adesc = sm100::make_smem_desc(abase, 2048u, 128u);
                             for (int kc = 0; kc < nch; kc += cps) {
                                 const int cnt = min(cps, nch - kc);
                                 uint32_t stg;
@@ -247,28 +254,37 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                     sm100::tc_fence_after();
                                     stg = sW + s * kStageBytes;
                                 }
-                                for (int j = 0; j < cnt; ++j) {
-                                    const uint64_t adesc = sm100::make_smem_desc(abase + (kc + j) * 4096u, 2048u, 128u);
-                                    const uint32_t cb = stg + j * cbytes;
-                                    for (int n0 = 0; n0 < ly.N; n0 += 256) {
-                                        const int nn = ly.N - n0 < 256 ? ly.N - n0 : 256;
-                                        const uint64_t bdesc = sm100::make_smem_desc(cb + (n0 / 8) * 128u, lbo_b, 128u);
-                                        sm100::mma_i8(dcol + n0, adesc, bdesc,
-                                                      nn == 256 ? idesc_full : sm100::make_idesc_i8(nn),
-                                                      (kc + j) > 0 ? 1u : 0u);
+                                uint64_t bdesc = sm100::make_smem_desc(stg, cbytes >> 1, 128u);
+                                if (sm100::elect_one()) {
+                                    for (int j = 0; j < cnt; ++j) {
+                                        const uint32_t acc = (kc + j) > 0 ? 1u : 0u;
+                                        sm100::mma_i8(dcol, adesc, bdesc, idesc_a, acc);
+                                        if (ly.N > 256)  // second N half: B rows 256.., D columns 256..
+                                            sm100::mma_i8(dcol + 256, adesc, bdesc + (256u * 128u / 8u >> 4), idesc_b, acc);
+                                        adesc += 4096u >> 4;
+                                        bdesc += cbytes >> 4;
                                     }
+                                } else {
+                                    adesc += static_cast<uint64_t>(cnt) * (4096u >> 4);
                                 }
+                                __syncwarp();
                                 if (mode != kResident) {
-                                    sm100::mma_commit(&empty[s]);
+                                    if (sm100::elect_one())
+                                        sm100::mma_commit(&empty[s]);
+                                    __syncwarp();
                                     if (++s == p.stages) {
                                         s = 0;
                                         ph ^= 1u;
                                     }
                                 }
                             }
-                            sm100::mma_commit(&d_full[sl]);
-                            tr(30 + l + 4 * sl);
+                            if (sm100::elect_one())
+                                sm100::mma_commit(&d_full[sl]);
+                            __syncwarp();
+                            if (lane_id() == 0)
+                                tr(30 + l + 4 * sl);
                         }
+                    }
         }
     } else {
         // ------------------------------------------------ encode / epilogue / readout
@@ -577,6 +593,7 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
             MlpLayer &ly = p.layer[e][l];
             ly.K = K;
             ly.N = N;
+            ly.cps = std::max(1, kStageBytes / (N * kKChunk));
             ly.woff = static_cast<long long>(img.size());
             ly.boff = static_cast<int>(bias.size());
             // weight image: K/32 chunks of [2 halves][N/8 groups][8 rows][16 bytes]
