@@ -37,6 +37,7 @@ struct Args {
     std::size_t batch = 1024;
     long long timeout_us = 200;
     int gpus = 1;
+    bool immediate = false;  // AIDA*: evaluate inline on the searcher threads
 };
 
 std::vector<unsigned char> read_all(const std::string &p) {
@@ -133,7 +134,7 @@ int run(const Args &a) {
     if (a.mode == "both" || a.mode == "gpu")
         modes.push_back("gpu");
     for (const std::string &mode : modes) {
-        EvaluatorGroup<D> group(make_backends<D>(a, mode == "gpu"), a.batch, a.timeout_us);
+        EvaluatorGroup<D> group(make_backends<D>(a, mode == "gpu"), a.batch, a.timeout_us, a.immediate);
         for (int i = a.first; i < static_cast<int>(insts.size()) && i < a.first + a.count; ++i) {
             const SearchResult<D> r = batch_idastar<D>(insts[static_cast<std::size_t>(i)], group, cfg);
             const SearchStats &s = r.stats;
@@ -155,7 +156,8 @@ int run(const Args &a) {
                    << it.batches << ", " << it.batch_items << "]";
             }
             js << "], \"threads\": " << a.threads << ", \"work_num\": " << a.work_num << ", \"batch\": " << a.batch
-               << ", \"timeout_us\": " << a.timeout_us << ", \"evaluators\": " << a.evaluators << "}";
+               << ", \"timeout_us\": " << a.timeout_us << ", \"evaluators\": " << a.evaluators
+               << ", \"immediate\": " << (a.immediate ? "true" : "false") << "}";
             std::printf("%s\n", js.str().c_str());
             std::fflush(stdout);
         }
@@ -196,6 +198,7 @@ int main(int argc, char **argv) {
         else if (k == "--time-limit") a.time_limit = std::stod(val());
         else if (k == "--first") a.first = std::stoi(val());
         else if (k == "--count") a.count = std::stoi(val());
+        else if (k == "--immediate") a.immediate = true;
         else {
             std::fprintf(stderr, "unknown flag %s\n", k.c_str());
             return 2;

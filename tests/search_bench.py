@@ -1,0 +1,73 @@
+"""Batch IDA* nodes/s with the B200 evaluator vs the reference CPU evaluator
+(BASELINE.json metric, second half).  Runs tests/cpp/bin/search_parity (the
+reference's own batch_idastar / aidastar with GpuBackend or
+LinearModelBackend dropped in) on Korf's 15-puzzle instances with the
+linear-Manhattan model and prints one JSON line
+per run.  Not a pytest test; results are committed under profiles/.
+
+    python tests/search_bench.py --instances 8,4 --threads 16
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+BIN = os.path.join(ROOT, "tests", "cpp", "bin", "search_parity")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--instances", default="8,4")  # korf10 indices (0-based): #9 cost 46, #5 cost 56
+    ap.add_argument("--threads", type=int, default=os.cpu_count() or 8)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    from oracle_lib import manhattan_linear_weights
+
+    import paper_2507_11916_b200 as bida
+
+    g = np.load(os.path.join(ROOT, "tests", "golden", "instances.npz"))
+    inst = "/tmp/korf10.txt"
+    with open(inst, "w") as f:
+        for v in g["korf10"]:
+            v = int(v)
+            f.write("stp 4 " + " ".join(str((v >> (4 * c)) & 15) for c in range(16)) + "\n")
+    blin = "/tmp/man4.blin"
+    open(blin, "wb").write(bida.blin1_bytes("stp4", manhattan_linear_weights(4, 72, 4.0), 72))
+    n = a.threads
+    runs = [
+        # (label, mode, extra args)
+        ("gpu batch_idastar E=1", "gpu", ["--evaluators", "1", "--work-num", "32", "--batch", "8192", "--timeout-us", "100"]),
+        ("gpu batch_idastar E=4", "gpu", ["--evaluators", "4", "--work-num", "32", "--batch", "4096", "--timeout-us", "100"]),
+        ("cpu batch_idastar E=n", "cpu", ["--evaluators", str(n), "--work-num", "8", "--batch", "256", "--timeout-us", "100"]),
+        ("cpu aidastar (immediate)", "cpu", ["--immediate", "--evaluators", "1", "--work-num", "1", "--batch", "1"]),
+    ]
+    lines = []
+    for idx in a.instances.split(","):
+        for label, mode, extra in runs:
+            cmd = [BIN, "--domain", "stp4", "--instances", inst, "--model", "linear:" + blin, "--mode", mode,
+                   "--threads", str(n), "--first", idx, "--count", "1", *extra]
+            out = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+            if out.returncode:
+                print(out.stderr, file=sys.stderr)
+                continue
+            for l in out.stdout.splitlines():
+                if l.startswith("{"):
+                    r = json.loads(l)
+                    r["label"] = label
+                    r.pop("iterations", None)
+                    lines.append(r)
+                    print(json.dumps(r), flush=True)
+    if a.out:
+        with open(a.out, "w") as f:
+            for r in lines:
+                f.write(json.dumps(r) + "\n")
+
+
+if __name__ == "__main__":
+    main()
