@@ -85,12 +85,20 @@ struct bida_gpu_evaluator {
     int32_t *d_h[2] = {nullptr, nullptr};
     int *err_host = nullptr; // mapped pinned, kErrWords ints
     int *err_dev = nullptr;
+    // small-batch zero-copy path: mapped pinned in/out read/written by the kernel
+    void *zc_in = nullptr, *zc_in_dev = nullptr;
+    int32_t *zc_out = nullptr, *zc_out_dev = nullptr;
+    std::atomic<int64_t> zc_calls{0};
     std::atomic<int64_t> launches{0};
 };
 
 namespace {
 
 constexpr int64_t kMaxSlot = int64_t(1) << 20;
+// Batches up to this size skip the copy engines: the kernel reads the packed
+// states from mapped pinned memory and writes h straight back into it (one
+// launch + one stream sync per call; search batches are 1-8K states).
+constexpr int64_t kZeroCopyMax = int64_t(1) << 15;
 
 template <int DOMAIN, int CS>
 int launch_linear_t(bida_gpu_evaluator *ev, const LinearArgs &a, cudaStream_t st) {
@@ -208,6 +216,10 @@ int common_init(bida_gpu_evaluator *ev, int device) {
                            cudaHostAllocMapped));
     std::memset(ev->err_host, 0, kErrWords * sizeof(int));
     CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&ev->err_dev), ev->err_host, 0));
+    CUDA_TRY(cudaHostAlloc(&ev->zc_in, kZeroCopyMax * 16, cudaHostAllocMapped | cudaHostAllocWriteCombined));
+    CUDA_TRY(cudaHostGetDevicePointer(&ev->zc_in_dev, ev->zc_in, 0));
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&ev->zc_out), kZeroCopyMax * 4, cudaHostAllocMapped));
+    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&ev->zc_out_dev), ev->zc_out, 0));
     return BIDA_OK;
 }
 
@@ -225,6 +237,8 @@ void release(bida_gpu_evaluator *ev) {
         if (ev->stream[s]) cudaStreamDestroy(ev->stream[s]);
     }
     if (ev->err_host) cudaFreeHost(ev->err_host);
+    if (ev->zc_in) cudaFreeHost(ev->zc_in);
+    if (ev->zc_out) cudaFreeHost(ev->zc_out);
     if (ev->d_Wt) cudaFree(ev->d_Wt);
     if (ev->d_rowflag) cudaFree(ev->d_rowflag);
     if (ev->mlp) mlp_destroy(ev->mlp);
@@ -467,6 +481,24 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         return BIDA_OK;
     std::lock_guard<std::mutex> lk(ev->mu);
     CUDA_TRY(cudaSetDevice(ev->device));
+    if (n <= kZeroCopyMax && !logits_out) {
+        const int pbz = packed_bytes(ev->domain);
+        std::memcpy(ev->zc_in, packed, static_cast<size_t>(n) * pbz);
+        int rc = launch(ev, ev->zc_in_dev, n, ev->zc_out_dev, nullptr, ev->stream[0]);
+        if (rc == BIDA_OK) {
+            const cudaError_t e = cudaStreamSynchronize(ev->stream[0]);
+            if (e != cudaSuccess)
+                rc = fail(BIDA_ERR_CUDA, std::string("evaluate: ") + cudaGetErrorString(e));
+        }
+        ev->zc_calls.fetch_add(1, std::memory_order_relaxed);
+        if (rc != BIDA_OK) {
+            std::fill(h_out, h_out + n, 0);
+            collect_errors(ev);
+            return rc;
+        }
+        std::memcpy(h_out, ev->zc_out, static_cast<size_t>(n) * 4);
+        return collect_errors(ev);
+    }
     if (int rc = ensure_slots(ev, n)) {
         std::fill(h_out, h_out + n, 0);
         return rc;

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -47,7 +48,8 @@ enum MlpMode { kPair = 0, kSplit = 1, kResident = 2 };
 
 struct MlpLayer {
     int K, N;          // padded input width (multiple of 32), output width (multiple of 16)
-    int cps;           // K-chunks per 16 KB stage (streaming modes)
+    int nh;            // N-halves streamed/computed separately (split schedule hidden layers: 2)
+    int cps;           // K-chunks (of one N-half) per 16 KB stage (streaming modes)
     int shift;         // hidden layers
     int boff;          // bias offset (int32 elements, multiple of 4)
     long long woff;    // weight image offset (bytes)
@@ -95,12 +97,6 @@ thread_local std::string g_err;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
-// K-chunks (32 B of K each) carried by one 16 KB stage for a layer with N outputs.
-__device__ __forceinline__ int chunks_per_stage(int N) {
-    const int c = kStageBytes / (N * kKChunk);
-    return c < 1 ? 1 : c;
-}
-
 // Debug timeline: lane 0 of each warp of CTA 0 appends (clock64 << 8 | tag).
 struct Tracer {
     long long *buf = nullptr;
@@ -140,7 +136,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
     uint64_t *d_full = act_ready + 2;            // [2]
     uint64_t *x_ready = d_full + 2;              // resident: one-hot of the next job written
     uint64_t *w_ready = x_ready + 1;             // resident: weight image landed
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w_ready + 1);
+    uint64_t *o_full = w_ready + 1;              // split: output-layer accumulator ready
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_full + 1);
 
     const int warp = threadIdx.x >> 5;
     const long long ntiles = (p.n + kTileM - 1) / kTileM;
@@ -153,11 +150,12 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             sm100::mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
-            sm100::mbar_init(&act_ready[s], mode == kPair ? 128 : 256);
+            sm100::mbar_init(&act_ready[s], mode == kResident ? 256 : 128);
             sm100::mbar_init(&d_full[s], 1);
         }
         sm100::mbar_init(x_ready, 128);
         sm100::mbar_init(w_ready, 1);
+        sm100::mbar_init(o_full, 1);
         sm100::fence_barrier_init();
     }
     if (warp == 1)
@@ -189,19 +187,20 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                             for (int sl = 0; sl < per && k0 + sl < nloc; ++sl) {
                                 const MlpLayer &ly = p.layer[e][l];
                                 const int nch = ly.K / kKChunk, cps = ly.cps;
-                                const uint32_t cbytes = static_cast<uint32_t>(ly.N) * kKChunk;
-                                for (int kc = 0; kc < nch; kc += cps) {
-                                    const int cnt = min(cps, nch - kc);
-                                    sm100::mbar_wait(&empty[s], ph ^ 1u);
-                                    sm100::mbar_arrive_expect_tx(&full[s], cnt * cbytes);
-                                    sm100::bulk_g2s(wbuf + s * kStageBytes,
-                                                    p.wimg + ly.woff + static_cast<size_t>(kc) * cbytes, cnt * cbytes,
-                                                    &full[s]);
-                                    if (++s == p.stages) {
-                                        s = 0;
-                                        ph ^= 1u;
+                                const uint32_t cbytes = static_cast<uint32_t>(ly.N / ly.nh) * kKChunk;
+                                for (int h = 0; h < ly.nh; ++h)
+                                    for (int kc = 0; kc < nch; kc += cps) {
+                                        const int cnt = min(cps, nch - kc);
+                                        sm100::mbar_wait(&empty[s], ph ^ 1u);
+                                        sm100::mbar_arrive_expect_tx(&full[s], cnt * cbytes);
+                                        sm100::bulk_g2s(wbuf + s * kStageBytes,
+                                                        p.wimg + ly.woff + static_cast<size_t>(h * nch + kc) * cbytes,
+                                                        cnt * cbytes, &full[s]);
+                                        if (++s == p.stages) {
+                                            s = 0;
+                                            ph ^= 1u;
+                                        }
                                     }
-                                }
                             }
             }
         }
@@ -209,7 +208,80 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
         // ------------------------------------------------ MMA issuer
         // The whole warp walks the schedule (uniform control flow, descriptors
         // in uniform registers); one elected lane issues the tcgen05 ops.
-        if (nloc > 0) {
+        if (nloc > 0 && mode == kSplit) {
+            // N-half pipelined schedule: half h of a hidden layer is committed to
+            // d_full[h] and drained by group h while the MMAs of the other half
+            // (or of the next layer's first K half) run; K-chunks below nch/2 of
+            // the next layer need only group 0's output (act_ready[0]).
+            int s = 0;
+            uint32_t ph = 0, aph[2] = {0u, 0u};
+            const uint32_t sbase = sm100::smem_u32(smem), sW = sm100::smem_u32(wbuf);
+            for (long long k0 = 0; k0 < nloc; ++k0)
+                for (int e = 0; e < p.E; ++e) {
+                    int prev_half = 0;  // columns group 0 drained in the previous layer (0 = none)
+                    for (int l = 0; l < p.nl; ++l) {
+                        const MlpLayer ly = p.layer[e][l];
+                        const int nch = ly.K / kKChunk, cps = ly.cps, Nh = ly.N / ly.nh;
+                        const uint32_t cbytes = static_cast<uint32_t>(Nh) * kKChunk;
+                        const uint32_t idesc = sm100::make_idesc_i8(Nh);
+                        const uint32_t abase = sbase + ((l & 1) ? p.xbytes : 0);
+                        const int split = nch / 2;  // K-chunks [0, split) come from group 0
+                        if (lane_id() == 0)
+                            tr(10 + l);
+                        sm100::mbar_wait(&act_ready[0], aph[0]);
+                        aph[0] ^= 1u;
+                        bool have1 = false;
+                        // TMEM hazard: this layer's first half writes beyond what group 0 drained
+                        if (split == 0 || (prev_half > 0 && Nh > prev_half)) {
+                            sm100::mbar_wait(&act_ready[1], aph[1]);
+                            aph[1] ^= 1u;
+                            have1 = true;
+                        }
+                        if (lane_id() == 0)
+                            tr(20 + l);
+                        sm100::tc_fence_after();
+                        for (int h = 0; h < ly.nh; ++h) {
+                            const uint32_t dcol = tmem + h * Nh;
+                            uint64_t adesc = sm100::make_smem_desc(abase, 2048u, 128u);
+                            for (int kc = 0; kc < nch; kc += cps) {
+                                const int cnt = min(cps, nch - kc);
+                                if (!have1 && kc + cnt > split) {
+                                    sm100::mbar_wait(&act_ready[1], aph[1]);
+                                    aph[1] ^= 1u;
+                                    have1 = true;
+                                    sm100::tc_fence_after();
+                                }
+                                sm100::mbar_wait(&full[s], ph);
+                                sm100::tc_fence_after();
+                                uint64_t bdesc = sm100::make_smem_desc(sW + s * kStageBytes, cbytes >> 1, 128u);
+                                if (sm100::elect_one()) {
+                                    for (int j = 0; j < cnt; ++j) {
+                                        sm100::mma_i8(dcol, adesc, bdesc, idesc, (kc + j) > 0 ? 1u : 0u);
+                                        adesc += 4096u >> 4;
+                                        bdesc += cbytes >> 4;
+                                    }
+                                } else {
+                                    adesc += static_cast<uint64_t>(cnt) * (4096u >> 4);
+                                }
+                                __syncwarp();
+                                if (sm100::elect_one())
+                                    sm100::mma_commit(&empty[s]);
+                                __syncwarp();
+                                if (++s == p.stages) {
+                                    s = 0;
+                                    ph ^= 1u;
+                                }
+                            }
+                            if (sm100::elect_one())
+                                sm100::mma_commit(l + 1 < p.nl ? &d_full[h] : o_full);
+                            __syncwarp();
+                        }
+                        if (lane_id() == 0)
+                            tr(30 + l);
+                        prev_half = ly.N / 2;
+                    }
+                }
+        } else if (nloc > 0) {
             int s = 0;
             uint32_t ph = 0, aph[2] = {0u, 0u}, xph = 0;
             const uint32_t sbase = sm100::smem_u32(smem), sW = sm100::smem_u32(wbuf);
@@ -294,14 +366,15 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
         const int sl = mode == kPair ? grp : 0;
         const uint32_t sX = sm100::smem_u32(smem) + sl * set_bytes;
         const uint32_t sY = sX + p.xbytes;
-        uint64_t *my_ready = &act_ready[sl];
-        uint64_t *my_full = &d_full[sl];
-        uint32_t dph = 0;
+        // split: group g owns act_ready[g] / d_full[g] (its K half / N half)
+        uint64_t *my_ready = &act_ready[mode == kSplit ? grp : sl];
+        uint64_t *my_full = &d_full[mode == kSplit ? grp : sl];
+        uint32_t dph = 0, oph = 0;
         // pair: this group's own tiles; split/resident: every tile of the CTA
         const long long kfirst = mode == kPair ? grp : 0, kstep = mode == kPair ? 2 : 1;
         // who encodes / reads out: pair -> both groups (own tiles); split -> group 0;
         // resident -> group 1 encodes (one job ahead), group 0 reads out
-        const bool encoder = mode == kPair || (mode == kSplit ? grp == 0 : grp == 1);
+        const bool encoder = mode == kPair || mode == kSplit || grp == 1;
         const bool reader = mode == kPair || grp == 0;
 
         auto load_state = [&](long long kk, uint64_t &lo_, uint64_t &hi_) {
@@ -327,15 +400,21 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             return b;
         };
         // one-hot row of a packed state into X (layer 0's A operand), then publish
+        // split: group g writes only its K half of the one-hot (16-byte chunks
+        // [c_lo, c_hi)), aligned with the MMA's K split at (Fpad/32)/2 chunks of 32 B
+        const int c16_split = 2 * ((p.Fpad / 32) / 2);
+        const int c_lo = mode == kSplit && grp == 1 ? c16_split : 0;
+        const int c_hi = mode == kSplit && grp == 0 ? c16_split : p.Fpad / 16;
         auto encode = [&](uint64_t lo_, uint64_t hi_, bool live_, uint64_t *bar) {
             tr(40);
-            for (int c16 = 0; c16 < p.Fpad / 16; ++c16)
+            for (int c16 = c_lo; c16 < c_hi; ++c16)
                 sm100::st_shared_v4(sX + c16 * 2048u + row * 16u, 0u, 0u, 0u, 0u);
             if (live_) {
 #pragma unroll
                 for (int q = 0; q < T::NNZ; ++q) {
                     const int j = position_feature<DOMAIN>(lo_, hi_, q);
-                    sm100::st_shared_u8(sX + (j >> 4) * 2048u + row * 16u + (j & 15), 1u);
+                    if ((j >> 4) >= c_lo && (j >> 4) < c_hi)
+                        sm100::st_shared_u8(sX + (j >> 4) * 2048u + row * 16u + (j & 15), 1u);
                 }
             }
             sm100::fence_proxy_async_smem();
@@ -372,9 +451,14 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                 for (int l = 0; l < p.nl; ++l) {
                     const MlpLayer &ly = p.layer[e][l];
                     tr(50 + l);
-                    sm100::mbar_wait(my_full, dph);
+                    if (mode == kSplit && l + 1 == p.nl) {
+                        sm100::mbar_wait(o_full, oph);
+                        oph ^= 1u;
+                    } else {
+                        sm100::mbar_wait(my_full, dph);
+                        dph ^= 1u;
+                    }
                     tr(60 + l);
-                    dph ^= 1u;
                     sm100::tc_fence_after();
                     const int32_t *bias = p.bias + ly.boff;
                     if (l + 1 < p.nl) {
@@ -577,6 +661,12 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     }
     std::vector<uint8_t> img;
     std::vector<int32_t> bias;
+    struct WSrc {
+        const int8_t *W;
+        int in, outn;
+    };
+    std::vector<WSrc> wsrc;  // [e][l]
+    size_t wtotal = 0;
     for (uint32_t e = 0; e < E; ++e) {
         for (int l = 0; l < nl; ++l) {
             const int in = l ? H[l - 1] : F;
@@ -593,22 +683,9 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
             MlpLayer &ly = p.layer[e][l];
             ly.K = K;
             ly.N = N;
-            ly.cps = std::max(1, kStageBytes / (N * kKChunk));
-            ly.woff = static_cast<long long>(img.size());
+            wtotal += static_cast<size_t>(N) * K;
             ly.boff = static_cast<int>(bias.size());
-            // weight image: K/32 chunks of [2 halves][N/8 groups][8 rows][16 bytes]
-            const size_t base = img.size();
-            img.resize(base + static_cast<size_t>(N) * K, 0);
-            for (int kc = 0; kc < K / 32; ++kc)
-                for (int n = 0; n < outn; ++n)
-                    for (int k = 0; k < 32; ++k) {
-                        const int kk = kc * 32 + k;
-                        if (kk >= in)
-                            continue;
-                        const size_t pos = base + static_cast<size_t>(kc) * N * 32 + (k / 16) * (N * 16) +
-                                           (n / 8) * 128 + (n % 8) * 16 + (k % 16);
-                        img[pos] = static_cast<uint8_t>(W[static_cast<size_t>(n) * in + kk]);
-                    }
+            wsrc.push_back({W, in, outn});  // image written once the schedule is known
             for (int n = 0; n < N; ++n) {
                 int32_t v = 0;
                 if (n < outn)
@@ -652,7 +729,7 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     p.rk.uHi = std::nextafter(static_cast<float>(u + eps64), INFINITY);
     p.xbytes = kTileM * KX;
     p.ybytes = kTileM * KY;
-    p.wbytes = static_cast<int>(img.size());
+    p.wbytes = static_cast<int>(wtotal);
     p.wbytes_pad = (p.wbytes + 1023) & ~1023;
     const size_t bar_bytes = 8 * (2 * kMaxStages + 6) + 16;
     const size_t budget = 227 * 1024;
@@ -672,12 +749,18 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     //    activation set: resident
     // 2) every layer <= 256 wide and two activation sets fit: pair (streamed)
     // 3) otherwise: split (streamed)
-    if (Nmax <= 256 && set1 + p.wbytes_pad + bar_bytes <= budget) {  // (TMEM double-buffered by job)
+    // BIDA_MLP_FORCE_MODE=resident|pair|split (tests): use that schedule when it fits
+    const char *force = std::getenv("BIDA_MLP_FORCE_MODE");
+    const std::string fm = force ? force : "";
+    const bool fit_res = Nmax <= 256 && set1 + p.wbytes_pad + bar_bytes <= budget;
+    const bool fit_pair = Nmax <= 256 && stages_for(2 * set1) >= 2;
+    const bool want_split = fm == "split" && stages_for(set1) >= 2;
+    if (!want_split && fit_res && (fm.empty() || fm == "resident" || (fm == "pair" && !fit_pair))) {  // (TMEM double-buffered by job)
         p.mode = kResident;
         p.stages = 0;
         p.tmem_cols = 512u;
         m->smem = set1 + p.wbytes_pad + bar_bytes;
-    } else if (Nmax <= 256 && stages_for(2 * set1) >= 2) {
+    } else if (!want_split && fit_pair) {
         p.mode = kPair;
         p.stages = stages_for(2 * set1);
         p.tmem_cols = 512;
@@ -690,6 +773,38 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     } else {
         delete m;
         return fail(err, 1, "BMLP1: model too wide for shared memory");
+    }
+    // Weight image, per layer in MMA consumption order: nh N-halves (2 for the
+    // split schedule's hidden layers, else 1), each K/32 chunks of
+    // [2 K-halves][N/nh/8 row groups][8 rows][16 bytes] (UMMA K-major, no swizzle).
+    img.assign(wtotal, 0);
+    {
+        size_t pos0 = 0;
+        for (int e = 0; e < static_cast<int>(E); ++e)
+            for (int l = 0; l < nl; ++l) {
+                MlpLayer &ly = p.layer[e][l];
+                const WSrc &w = wsrc[static_cast<size_t>(e) * nl + l];
+                ly.nh = (p.mode == kSplit && l + 1 < nl) ? 2 : 1;
+                const int Nh = ly.N / ly.nh;
+                ly.cps = std::max(1, kStageBytes / (Nh * kKChunk));
+                ly.woff = static_cast<long long>(pos0);
+                for (int h = 0; h < ly.nh; ++h)
+                    for (int kc = 0; kc < ly.K / 32; ++kc)
+                        for (int nn = 0; nn < Nh; ++nn) {
+                            const int n = h * Nh + nn;
+                            if (n >= w.outn)
+                                continue;
+                            for (int k = 0; k < 32; ++k) {
+                                const int kk = kc * 32 + k;
+                                if (kk >= w.in)
+                                    continue;
+                                const size_t pos = pos0 + (static_cast<size_t>(h) * (ly.K / 32) + kc) * Nh * 32 +
+                                                   (k / 16) * (Nh * 16) + (nn / 8) * 128 + (nn % 8) * 16 + (k % 16);
+                                img[pos] = static_cast<uint8_t>(w.W[static_cast<size_t>(n) * w.in + kk]);
+                            }
+                        }
+                pos0 += static_cast<size_t>(ly.N) * ly.K;
+            }
     }
     m->cm = C <= 32 ? 32 : (C <= 64 ? 64 : 256);
     m->grid_cap = num_sms;

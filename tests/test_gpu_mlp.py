@@ -125,3 +125,18 @@ def test_bad_models_rejected():
         bida.MlpModelBackend("rc", b"BMLP1" + b"\0" * 8, 0.5)
     with pytest.raises(RuntimeError):
         bida.MlpModelBackend("stp4", make_bmlp1("rc", hidden=[64], classes=21, seed=1), 0.5)
+
+
+@pytest.mark.parametrize("schedule", ["resident", "pair", "split"])
+@pytest.mark.parametrize(
+    "hidden,C,E",
+    [([128, 128], 21, 1), ([96, 160], 21, 1), ([64, 256, 96], 27, 2), ([256, 64], 40, 1), ([32], 7, 3)],
+)
+def test_every_schedule_matches_oracle(orc, monkeypatch, schedule, hidden, C, E):
+    """The three kernel schedules (resident weights / tile ping-pong / N-half
+    pipelined split) give identical, oracle-exact results, including odd
+    K-chunk splits (96, 160) and layers wider than the previous one."""
+    monkeypatch.setenv("BIDA_MLP_FORCE_MODE", schedule)
+    blob = make_bmlp1("rc", hidden=hidden, classes=C, ensemble=E, seed=len(hidden) * 100 + C)
+    packed = bida.random_walks("rc", 777, 0, 30, seed=C + E)
+    check(orc, RC, blob, 0.5, packed, E, C)
