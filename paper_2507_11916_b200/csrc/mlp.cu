@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                         aph[0] ^= 1u;
                         bool have1 = false;
                         // TMEM hazard: this layer's first half writes beyond what group 0 drained
-                        if (split == 0 || (prev_half > 0 && Nh > prev_half)) {
+                        if (l == 0 || split == 0 || (prev_half > 0 && Nh > prev_half)) {
                             sm100::mbar_wait(&act_ready[1], aph[1]);
                             aph[1] ^= 1u;
                             have1 = true;
@@ -374,7 +374,9 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
         const long long kfirst = mode == kPair ? grp : 0, kstep = mode == kPair ? 2 : 1;
         // who encodes / reads out: pair -> both groups (own tiles); split -> group 0;
         // resident -> group 1 encodes (one job ahead), group 0 reads out
-        const bool encoder = mode == kPair || mode == kSplit || grp == 1;
+        // split: group 1 encodes job j+1 while group 0 reads out job j; group 0
+        // releases TMEM (act_ready[0]) as soon as it has loaded job j's logits
+        const bool encoder = mode == kPair || grp == 1;
         const bool reader = mode == kPair || grp == 0;
 
         auto load_state = [&](long long kk, uint64_t &lo_, uint64_t &hi_) {
@@ -400,11 +402,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             return b;
         };
         // one-hot row of a packed state into X (layer 0's A operand), then publish
-        // split: group g writes only its K half of the one-hot (16-byte chunks
-        // [c_lo, c_hi)), aligned with the MMA's K split at (Fpad/32)/2 chunks of 32 B
-        const int c16_split = 2 * ((p.Fpad / 32) / 2);
-        const int c_lo = mode == kSplit && grp == 1 ? c16_split : 0;
-        const int c_hi = mode == kSplit && grp == 0 ? c16_split : p.Fpad / 16;
+        // (the split schedule's one-hot is written whole by group 1; see below)
+        const int c_lo = 0, c_hi = p.Fpad / 16;
         auto encode = [&](uint64_t lo_, uint64_t hi_, bool live_, uint64_t *bar) {
             tr(40);
             for (int c16 = c_lo; c16 < c_hi; ++c16)
@@ -445,8 +444,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                 if (mode != kResident) {
                     if (encoder)
                         encode(lo, hi, live, my_ready);
-                    else
-                        sm100::mbar_arrive(my_ready);
+                    else if (mode != kSplit || job == kfirst * p.E)
+                        sm100::mbar_arrive(my_ready);  // split: later jobs arrive at the previous readout
                 }
                 for (int l = 0; l < p.nl; ++l) {
                     const MlpLayer &ly = p.layer[e][l];
@@ -532,6 +531,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                 }
                             }
                             sm100::tc_fence_before();
+                            if (mode == kSplit && (e + 1 < p.E || k + 1 < nloc))
+                                sm100::mbar_arrive(my_ready);  // TMEM free: next job's layer 0 may start
                             tr(81);
                             if (p.logits_out && valid) {
                                 double *dst = p.logits_out + (static_cast<size_t>(st) * p.E + e) * p.C;
