@@ -65,6 +65,7 @@ struct MlpParams {
     ReadoutConsts rk;
     uint32_t tmem_cols;
     int mode;           // MlpMode
+    int cluster;        // 2: CTA pairs share weight stages by TMA multicast (streaming modes)
     int stages;         // weight ring depth (16 KB stages), streaming modes
     int wbytes, wbytes_pad;  // weight image bytes (resident mode)
     int xbytes, ybytes; // activation buffers per slot (even / odd layer inputs)
@@ -141,13 +142,19 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
 
     const int warp = threadIdx.x >> 5;
     const long long ntiles = (p.n + kTileM - 1) / kTileM;
-    const long long nloc = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    // CTA pairs (p.cluster == 2) stream the weights together, so both CTAs of a
+    // pair run the same number of tile iterations (the pair's even CTA has the
+    // larger share); surplus iterations of the odd CTA are empty tiles.
+    const bool mc = p.cluster == 2;
+    const uint32_t crank = mc ? sm100::cluster_rank() : 0u;
+    const long long b0 = static_cast<long long>(blockIdx.x) - crank;
+    const long long nloc = b0 < ntiles ? (ntiles - b0 + gridDim.x - 1) / gridDim.x : 0;
     const bool tdbl = p.tmem_cols == 512u;  // TMEM halves available for double-buffering
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kMaxStages; ++s) {
             sm100::mbar_init(&full[s], 1);
-            sm100::mbar_init(&empty[s], 1);
+            sm100::mbar_init(&empty[s], mc ? 2 : 1);  // both CTAs' MMAs release a shared stage
         }
         for (int s = 0; s < 2; ++s) {
             sm100::mbar_init(&act_ready[s], mode == kResident ? 256 : 128);
@@ -162,6 +169,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
         sm100::tmem_alloc(tmem_slot, p.tmem_cols);
     sm100::tc_fence_before();
     __syncthreads();
+    if (mc)
+        sm100::cluster_sync();  // peer barriers initialised before any multicast lands
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     Tracer tr;
@@ -180,7 +189,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             } else {
                 const int per = mode == kPair ? 2 : 1;
                 int s = 0;
-                uint32_t ph = 0;
+                uint32_t ph = 0, g = 0;  // g: global stage counter (multicast: CTA g%2 issues)
                 for (long long k0 = 0; k0 < nloc; k0 += per)
                     for (int e = 0; e < p.E; ++e)
                         for (int l = 0; l < p.nl; ++l)
@@ -193,9 +202,12 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                         const int cnt = min(cps, nch - kc);
                                         sm100::mbar_wait(&empty[s], ph ^ 1u);
                                         sm100::mbar_arrive_expect_tx(&full[s], cnt * cbytes);
-                                        sm100::bulk_g2s(wbuf + s * kStageBytes,
-                                                        p.wimg + ly.woff + static_cast<size_t>(h * nch + kc) * cbytes,
-                                                        cnt * cbytes, &full[s]);
+                                        const uint8_t *src = p.wimg + ly.woff + static_cast<size_t>(h * nch + kc) * cbytes;
+                                        if (!mc)
+                                            sm100::bulk_g2s(wbuf + s * kStageBytes, src, cnt * cbytes, &full[s]);
+                                        else if ((g & 1u) == crank)
+                                            sm100::bulk_g2s_mc(wbuf + s * kStageBytes, src, cnt * cbytes, &full[s], 0x3);
+                                        ++g;
                                         if (++s == p.stages) {
                                             s = 0;
                                             ph ^= 1u;
@@ -265,7 +277,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                 }
                                 __syncwarp();
                                 if (sm100::elect_one())
-                                    sm100::mma_commit(&empty[s]);
+                                    (mc ? sm100::mma_commit_mc(&empty[s], 0x3) : sm100::mma_commit(&empty[s]));
                                 __syncwarp();
                                 if (++s == p.stages) {
                                     s = 0;
@@ -342,7 +354,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                 __syncwarp();
                                 if (mode != kResident) {
                                     if (sm100::elect_one())
-                                        sm100::mma_commit(&empty[s]);
+                                        (mc ? sm100::mma_commit_mc(&empty[s], 0x3) : sm100::mma_commit(&empty[s]));
                                     __syncwarp();
                                     if (++s == p.stages) {
                                         s = 0;
@@ -569,6 +581,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
     __syncwarp();  // reconverge the single-thread roles before the aligned barrier
     sm100::tc_fence_before();
     __syncthreads();
+    if (mc)
+        sm100::cluster_sync();  // no multicast or remote commit may target an exited CTA
     sm100::tc_fence_after();
     if (warp == 1)
         sm100::tmem_dealloc(tmem, p.tmem_cols);
@@ -597,9 +611,27 @@ int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
         return 1;
     }
     const long long ntiles = (p.n + kTileM - 1) / kTileM;
-    const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(ntiles, m->grid_cap)));
-    kern<<<grid, kMlpThreads, m->smem, st>>>(p);
-    e = cudaGetLastError();
+    int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(ntiles, m->grid_cap)));
+    if (p.cluster == 2) {
+        grid = (grid + 1) & ~1;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kMlpThreads);
+        cfg.dynamicSmemBytes = m->smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, p);
+    } else {
+        kern<<<grid, kMlpThreads, m->smem, st>>>(p);
+    }
+    if (e == cudaSuccess)
+        e = cudaGetLastError();
     if (e != cudaSuccess) {
         g_err = std::string("mlp launch: ") + cudaGetErrorString(e);
         return 1;
@@ -807,6 +839,10 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
                 pos0 += static_cast<size_t>(ly.N) * ly.K;
             }
     }
+    // streaming schedules pair CTAs to halve each SM's weight-stream load
+    // (BIDA_MLP_NO_MULTICAST=1 disables, for A/B measurements and tests)
+    const char *nomc = std::getenv("BIDA_MLP_NO_MULTICAST");
+    p.cluster = (p.mode != kResident && !(nomc && nomc[0] == '1')) ? 2 : 1;
     m->cm = C <= 32 ? 32 : (C <= 64 ? 64 : 256);
     m->grid_cap = num_sms;
     cudaError_t ce = cudaMalloc(&m->d_wimg, img.size());
