@@ -839,10 +839,12 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
                 pos0 += static_cast<size_t>(ly.N) * ly.K;
             }
     }
-    // streaming schedules pair CTAs to halve each SM's weight-stream load
-    // (BIDA_MLP_NO_MULTICAST=1 disables, for A/B measurements and tests)
-    const char *nomc = std::getenv("BIDA_MLP_NO_MULTICAST");
-    p.cluster = (p.mode != kResident && !(nomc && nomc[0] == '1')) ? 2 : 1;
+    // BIDA_MLP_MULTICAST=1: streaming schedules run as CTA pairs sharing weight
+    // stages by TMA multicast.  Off by default: measured slower on B200 (h512
+    // 1.16 vs 1.26 G evals/s) -- the pair's lockstep costs more than the halved
+    // per-SM copy issue saves (profiles/r1_notes.md).
+    const char *mcv = std::getenv("BIDA_MLP_MULTICAST");
+    p.cluster = (p.mode != kResident && mcv && mcv[0] == '1') ? 2 : 1;
     m->cm = C <= 32 ? 32 : (C <= 64 ? 64 : 256);
     m->grid_cap = num_sms;
     cudaError_t ce = cudaMalloc(&m->d_wimg, img.size());

@@ -145,11 +145,11 @@ def test_every_schedule_matches_oracle(orc, monkeypatch, schedule, hidden, C, E)
 @pytest.mark.parametrize("multicast", ["0", "1"])
 @pytest.mark.parametrize("schedule,hidden", [("pair", [256, 256]), ("split", [512, 512]), ("split", [96, 160])])
 def test_cluster_multicast_on_and_off(orc, monkeypatch, multicast, schedule, hidden):
-    """Streaming schedules run as CTA pairs sharing weight stages by TMA
-    multicast; the single-CTA path (BIDA_MLP_NO_MULTICAST=1) must agree.
+    """Streaming schedules optionally run as CTA pairs sharing weight stages by
+    TMA multicast (BIDA_MLP_MULTICAST=1); both paths must agree with the oracle.
     1001 states -> 8 tiles: pairs whose odd CTA gets an empty surplus tile."""
     monkeypatch.setenv("BIDA_MLP_FORCE_MODE", schedule)
-    monkeypatch.setenv("BIDA_MLP_NO_MULTICAST", "1" if multicast == "0" else "0")
+    monkeypatch.setenv("BIDA_MLP_MULTICAST", multicast)
     blob = make_bmlp1("rc", hidden=hidden, classes=21, ensemble=1, seed=sum(hidden))
     for n in (1001, 148 * 128 * 2 + 77):
         packed = bida.random_walks("rc", n, 0, 30, seed=n)
