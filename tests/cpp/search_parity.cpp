@@ -38,7 +38,51 @@ struct Args {
     long long timeout_us = 200;
     int gpus = 1;
     bool immediate = false;  // AIDA*: evaluate inline on the searcher threads
+    int table1_corners = 0;  // >0: "Table-1" mode with an N-corner PDB (Rubik's)
 };
+
+// Table-1 mode: the network is evaluated for
+// every node (its cost is real) but the search is guided by the admissible
+// PDB value, so CPU and GPU runs expand identical trees.  `pdb_only` skips the
+// network (the AIDA*-with-PDB baseline).
+template <class D>
+class Table1Backend final : public EvaluatorBackend<D> {
+public:
+    Table1Backend(std::unique_ptr<EvaluatorBackend<D>> nn, std::shared_ptr<const Heuristic<D>> pdb)
+        : nn_(std::move(nn)), pdb_(std::move(pdb)) {}
+    bool needs_features() const override { return nn_ && nn_->needs_features(); }
+    void evaluate(std::span<const BatchItem<D>> batch, std::span<std::int32_t> out) override {
+        if (nn_)
+            nn_->evaluate(batch, out);  // h_NN computed (and discarded, as in the paper)
+        for (std::size_t i = 0; i < batch.size(); ++i)
+            out[i] = static_cast<std::int32_t>(pdb_->lookup(batch[i].state));
+    }
+
+private:
+    std::unique_ptr<EvaluatorBackend<D>> nn_;
+    std::shared_ptr<const Heuristic<D>> pdb_;
+};
+
+template <class D>
+std::shared_ptr<const Heuristic<D>> corner_pdb(int corners) {
+    if constexpr (std::is_same_v<D, RubiksCube>) {
+        std::vector<std::uint8_t> pat;
+        for (int c = 0; c < corners; ++c)
+            pat.push_back(static_cast<std::uint8_t>(c));
+        const std::string cache = "/tmp/bida_rc_corner" + std::to_string(corners) + ".pdb";
+        std::shared_ptr<const PdbTable<D>> t;
+        try {
+            t = std::make_shared<const PdbTable<D>>(PdbTable<D>::load(cache));
+        } catch (const std::exception &) {
+            auto built = PdbTable<D>::build(pat, D::solved());
+            built.save(cache);
+            t = std::make_shared<const PdbTable<D>>(std::move(built));
+        }
+        return std::make_shared<const PdbHeuristic<D>>(t);
+    } else {
+        throw std::runtime_error("--table1-pdb needs --domain rc");
+    }
+}
 
 std::vector<unsigned char> read_all(const std::string &p) {
     std::ifstream f(p, std::ios::binary);
@@ -70,6 +114,25 @@ private:
     orc_mlp m_{};
     double q_;
 };
+
+template <class D>
+std::vector<std::unique_ptr<EvaluatorBackend<D>>> make_backends(const Args &a, bool gpu);
+
+template <class D>
+std::vector<std::unique_ptr<EvaluatorBackend<D>>> make_mode_backends(const Args &a, const std::string &mode) {
+    if (a.table1_corners <= 0)
+        return make_backends<D>(a, mode == "gpu");
+    const auto pdb = corner_pdb<D>(a.table1_corners);
+    std::vector<std::unique_ptr<EvaluatorBackend<D>>> v;
+    if (mode == "pdb") {
+        for (int e = 0; e < a.evaluators; ++e)
+            v.push_back(std::make_unique<Table1Backend<D>>(nullptr, pdb));
+        return v;
+    }
+    for (auto &b : make_backends<D>(a, mode == "gpu"))
+        v.push_back(std::make_unique<Table1Backend<D>>(std::move(b), pdb));
+    return v;
+}
 
 template <class D>
 std::vector<std::unique_ptr<EvaluatorBackend<D>>> make_backends(const Args &a, bool gpu) {
@@ -133,8 +196,10 @@ int run(const Args &a) {
         modes.push_back("cpu");
     if (a.mode == "both" || a.mode == "gpu")
         modes.push_back("gpu");
+    if (a.mode == "pdb")
+        modes.push_back("pdb");
     for (const std::string &mode : modes) {
-        EvaluatorGroup<D> group(make_backends<D>(a, mode == "gpu"), a.batch, a.timeout_us, a.immediate);
+        EvaluatorGroup<D> group(make_mode_backends<D>(a, mode), a.batch, a.timeout_us, a.immediate);
         for (int i = a.first; i < static_cast<int>(insts.size()) && i < a.first + a.count; ++i) {
             const SearchResult<D> r = batch_idastar<D>(insts[static_cast<std::size_t>(i)], group, cfg);
             const SearchStats &s = r.stats;
@@ -157,7 +222,8 @@ int run(const Args &a) {
             }
             js << "], \"threads\": " << a.threads << ", \"work_num\": " << a.work_num << ", \"batch\": " << a.batch
                << ", \"timeout_us\": " << a.timeout_us << ", \"evaluators\": " << a.evaluators
-               << ", \"immediate\": " << (a.immediate ? "true" : "false") << "}";
+               << ", \"immediate\": " << (a.immediate ? "true" : "false")
+               << ", \"table1_corners\": " << a.table1_corners << "}";
             std::printf("%s\n", js.str().c_str());
             std::fflush(stdout);
         }
@@ -199,6 +265,7 @@ int main(int argc, char **argv) {
         else if (k == "--first") a.first = std::stoi(val());
         else if (k == "--count") a.count = std::stoi(val());
         else if (k == "--immediate") a.immediate = true;
+        else if (k == "--table1-pdb") a.table1_corners = std::stoi(val());
         else {
             std::fprintf(stderr, "unknown flag %s\n", k.c_str());
             return 2;

@@ -26,7 +26,12 @@ def main():
     ap.add_argument("--instances", default="8,4")  # korf10 indices (0-based): #9 cost 46, #5 cost 56
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 8)
     ap.add_argument("--out", default="")
+    ap.add_argument("--domain", default="stp4", choices=["stp4", "rc"])
+    ap.add_argument("--time-limit", type=float, default=30.0)
+    ap.add_argument("--walks", default="3:14:16:2507")  # rc: n:len_min:len_max:seed
     a = ap.parse_args()
+    if a.domain == "rc":
+        return rc_bench(a)
     from oracle_lib import manhattan_linear_weights
 
     import paper_2507_11916_b200 as bida
@@ -63,6 +68,45 @@ def main():
                     r.pop("iterations", None)
                     lines.append(r)
                     print(json.dumps(r), flush=True)
+    if a.out:
+        with open(a.out, "w") as f:
+            for r in lines:
+                f.write(json.dumps(r) + "\n")
+
+
+def rc_bench(a):
+    """Config 2 (BASELINE.json): Rubik's Batch IDA*, walks 14-16, BMLP1 480-128-128-21
+    evaluated per node on the GPU (or by the oracle on the CPU), search guided
+    by the reference's 5-corner PDB (Table-1 mode).  Each run is
+    time-limited; nodes/s is generated / wall."""
+    from paper_2507_11916_b200.models import make_bmlp1
+
+    model = "/tmp/m128.bmlp"
+    open(model, "wb").write(make_bmlp1("rc", hidden=[128, 128], classes=21, seed=2507))
+    n = a.threads
+    tl = str(a.time_limit)
+    runs = [
+        ("gpu batch_idastar nn+pdb E=1", "gpu", ["--evaluators", "1", "--work-num", "64", "--batch", "16384", "--timeout-us", "200"]),
+        ("gpu batch_idastar nn+pdb E=2", "gpu", ["--evaluators", "2", "--work-num", "64", "--batch", "8192", "--timeout-us", "200"]),
+        ("cpu batch_idastar nn+pdb E=n", "cpu", ["--evaluators", str(n), "--work-num", "8", "--batch", "512", "--timeout-us", "200"]),
+        ("cpu aidastar nn+pdb (immediate)", "cpu", ["--immediate", "--evaluators", "1", "--work-num", "1", "--batch", "1"]),
+        ("cpu aidastar pdb only (no nn)", "pdb", ["--immediate", "--evaluators", "1", "--work-num", "1", "--batch", "1"]),
+    ]
+    lines = []
+    for label, mode, extra in runs:
+        cmd = [BIN, "--domain", "rc", "--walks", a.walks, "--model", "mlp:" + model, "--mode", mode,
+               "--table1-pdb", "5", "--threads", str(n), "--time-limit", tl, *extra]
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=3600)
+        if out.returncode:
+            print(out.stderr, file=sys.stderr)
+            continue
+        for l in out.stdout.splitlines():
+            if l.startswith("{"):
+                r = json.loads(l)
+                r["label"] = label
+                r.pop("iterations", None)
+                lines.append(r)
+                print(json.dumps(r), flush=True)
     if a.out:
         with open(a.out, "w") as f:
             for r in lines:
