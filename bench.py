@@ -388,17 +388,27 @@ def main():
         peaks = _json.load(open(pk_path))
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     kern_s = r["kern_avg_ms"] / 1000.0
+    # DRAM traffic of the dominant kernel per launch, from the committed ncu
+    # --set full capture of this workload (profiles/traffic.json), scaled to B
+    traffic, traffic_src = None, None
+    tj = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tj):
+        t = _json.load(open(tj)).get(args.workload)
+        if t:
+            traffic = t["bytes_per_launch"] * B / t["states_per_launch"]
+            traffic_src = t["source"]
     if wl["kind"] == "linear":
         achieved = by * B / kern_s / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None,
+                "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                 "algorithmic_bytes_per_state": by}
     else:
         achieved = fl * B / kern_s / 1e12
         pk = peaks.get("bf16_tflops", 1590.0) * 2  # dense int8 = 2x dense bf16
         roof = {"bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
-                "frac": achieved / pk, "traffic": None, "flops_per_state": fl}
+                "frac": achieved / pk, "traffic": traffic, "traffic_source": traffic_src, "flops_per_state": fl,
+                "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x dense bf16 on B200)"}
     line = {
         "metric": "heuristic_evals_per_s",
         "value": value,
