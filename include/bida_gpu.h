@@ -116,6 +116,19 @@ int bida_gpu_evaluate_device(bida_gpu_evaluator *ev, const void *d_packed, int64
                              int32_t *d_h, double *d_logits, void *stream);
 int bida_gpu_stream_status(bida_gpu_evaluator *ev);
 
+/* PDB correction in the readout (north star "admissible class-argmax/PDB-
+ * correction readout"): h = min(h_model, h_PDB) (BIDA_PDB_MIN), or h = h_PDB
+ * with the model still evaluated (BIDA_PDB_REPLACE: the paper's Table-1 mode,
+ * PAPER.md:407).  h_PDB = PdbTable<D>::lookup (pdb.hpp:66-69) over the rank of
+ * Abstraction::rank_state (rubiks.hpp:247-267 corners, stp.hpp:208-227 tiles),
+ * computed on the device.  `entries` as PdbTable::entries(); the table is
+ * copied to device memory.  BIDA_PDB_OFF detaches. */
+enum bida_pdb_mode { BIDA_PDB_OFF = 0, BIDA_PDB_MIN = 1, BIDA_PDB_REPLACE = 2 };
+int bida_gpu_attach_pdb(bida_gpu_evaluator *ev, const uint8_t *pattern, int pattern_len,
+                        const uint8_t *entries, uint64_t n_entries, int mode);
+/* Same from a BPDB1 file written by PdbTable::save (pdb.hpp:78-96). */
+int bida_gpu_attach_pdb_file(bida_gpu_evaluator *ev, const char *path, int mode);
+
 int bida_gpu_info(const bida_gpu_evaluator *ev, bida_gpu_model_info *out);
 /* Diagnostics (MLP handles): record a clock64 timeline of CTA 0's warps into
  * the DEVICE buffer `dev_buf` (int64 [warps][bida_gpu_trace_slots()]) on every

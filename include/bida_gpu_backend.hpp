@@ -115,6 +115,15 @@ public:
         return std::unique_ptr<GpuBackend>(new GpuBackend(h));
     }
 
+    // PDB correction in the device readout (bida_gpu_attach_pdb_file):
+    // BIDA_PDB_MIN -> min(h_model, h_PDB); BIDA_PDB_REPLACE -> h_PDB with the
+    // model still evaluated (PAPER.md:407 Table-1 mode).  BPDB1 file from
+    // PdbTable::save (pdb.hpp:78-96).
+    void attach_pdb_file(const std::string &path, int mode) {
+        if (const int rc = bida_gpu_attach_pdb_file(handle_, path.c_str(), mode))
+            throw_status(rc, "GpuBackend::attach_pdb_file");
+    }
+
     ~GpuBackend() override {
         if (handle_)
             bida_gpu_destroy(handle_);

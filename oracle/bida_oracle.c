@@ -408,3 +408,74 @@ int orc_manhattan(int domain, const void *packed, int64_t n, int32_t *out) {
     }
     return ORC_OK;
 }
+
+/* ------------------------------------------------------------------ PDBs */
+
+/* partial_perm_rank (ranking.hpp:26-51): lexicographic rank of seq[0..m) among
+ * length-m sequences of distinct values from {0..n-1}.  -1 on repeats. */
+int64_t orc_partial_perm_rank(const int *seq, int m, int n) {
+    int64_t rank = 0;
+    for (int i = 0; i < m; ++i) {
+        int smaller = 0;
+        for (int j = 0; j < i; ++j) {
+            if (seq[j] == seq[i]) return -1;
+            if (seq[j] < seq[i]) ++smaller;
+        }
+        if (seq[i] < 0 || seq[i] >= n) return -1;
+        const int idx = seq[i] - smaller; /* index among the still-available values */
+        int64_t w = 1;
+        for (int a = 0; a < m - i - 1; ++a) w *= (int64_t)(n - i - 1 - a);
+        rank += (int64_t)idx * w;
+    }
+    return rank;
+}
+
+/* Abstraction::rank_state: RubiksCube corners (rubiks.hpp:247-267: pos/ori of
+ * each pattern corner, partial_perm_rank(pos, 8) then *3 + ori per corner) and
+ * TilePuzzle (stp.hpp:208-227: cell of each pattern tile, partial_perm_rank(pos,
+ * N*N)).  The last matching position wins, as in project().  -1 if invalid. */
+int64_t orc_pdb_rank(int domain, const uint8_t *pattern, int m, const void *packed) {
+    int pos[16], ori[16];
+    if (domain == ORC_RC) {
+        uint64_t lo;
+        memcpy(&lo, packed, 8);
+        for (int i = 0; i < m; ++i) {
+            pos[i] = -1;
+            ori[i] = 0;
+            for (int p = 0; p < 8; ++p)
+                if ((int)((lo >> (3 * p)) & 7) == pattern[i]) {
+                    pos[i] = p;
+                    ori[i] = (int)((lo >> (24 + 2 * p)) & 3);
+                }
+        }
+        int64_t r = orc_partial_perm_rank(pos, m, 8);
+        if (r < 0) return -1;
+        for (int i = 0; i < m; ++i) r = r * 3 + ori[i];
+        return r;
+    }
+    if (domain >= ORC_STP2 && domain <= ORC_STP4) {
+        const int K = domain * domain;
+        uint64_t v;
+        memcpy(&v, packed, 8);
+        for (int i = 0; i < m; ++i) {
+            pos[i] = -1;
+            for (int cell = 0; cell < K; ++cell)
+                if ((int)((v >> (4 * cell)) & 0xF) == pattern[i]) pos[i] = cell;
+        }
+        return orc_partial_perm_rank(pos, m, K);
+    }
+    return -1;
+}
+
+/* PdbTable::lookup (pdb.hpp:66-69): unreachable entries (0xFF) read as 0. */
+int orc_pdb_lookup(int domain, const uint8_t *pattern, int m, const uint8_t *entries, uint64_t n_entries,
+                   const void *packed, int64_t n, int32_t *out) {
+    const int pb = orc_packed_bytes(domain);
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t r = orc_pdb_rank(domain, pattern, m, (const char *)packed + i * pb);
+        if (r < 0 || (uint64_t)r >= n_entries) return ORC_ERR_ARG;
+        const uint8_t e = entries[r];
+        out[i] = e == 0xFF ? 0 : e;
+    }
+    return ORC_OK;
+}

@@ -54,3 +54,14 @@ int orc_manhattan(int domain, const void *packed, int64_t n, int32_t *out);
 #ifdef __cplusplus
 }
 #endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+int64_t orc_partial_perm_rank(const int *seq, int m, int n);
+int64_t orc_pdb_rank(int domain, const uint8_t *pattern, int m, const void *packed);
+int orc_pdb_lookup(int domain, const uint8_t *pattern, int m, const uint8_t *entries, uint64_t n_entries,
+                   const void *packed, int64_t n, int32_t *out);
+#ifdef __cplusplus
+}
+#endif

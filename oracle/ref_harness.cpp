@@ -371,3 +371,38 @@ extern "C" int ref_linear_run(void *prepared, std::int32_t *h_out, int threads) 
 }
 
 extern "C" void ref_linear_release(void *prepared) { delete static_cast<PreparedBase *>(prepared); }
+
+// ---- pattern databases (pdb.hpp:30-69), built and looked up by the reference ----
+extern "C" int ref_pdb_build(int domain, const std::uint8_t *pattern, int m, std::uint8_t *entries_out,
+                             std::uint64_t cap, std::uint64_t *n_out) {
+    return dispatch(domain, [&](auto *d) {
+        using D = bare_t<decltype(d)>;
+        std::vector<std::uint8_t> pat(pattern, pattern + m);
+        const PdbTable<D> t = PdbTable<D>::build(pat, D::solved());
+        *n_out = t.size();
+        if (t.size() > cap)
+            throw std::invalid_argument("PDB larger than the output buffer");
+        std::memcpy(entries_out, t.entries().data(), t.size());
+        return RH_OK;
+    });
+}
+
+extern "C" int ref_pdb_lookup_file(int domain, const char *path, const void *packed, std::int64_t n,
+                                   std::int32_t *out) {
+    return dispatch(domain, [&](auto *d) {
+        using D = bare_t<decltype(d)>;
+        const PdbTable<D> t = PdbTable<D>::load(path);
+        for (std::int64_t i = 0; i < n; ++i)
+            out[i] = t.lookup(unpack(d, static_cast<const char *>(packed) + i * packed_bytes<D>()));
+        return RH_OK;
+    });
+}
+
+extern "C" int ref_pdb_build_save(int domain, const std::uint8_t *pattern, int m, const char *path) {
+    return dispatch(domain, [&](auto *d) {
+        using D = bare_t<decltype(d)>;
+        std::vector<std::uint8_t> pat(pattern, pattern + m);
+        PdbTable<D>::build(pat, D::solved()).save(path);
+        return RH_OK;
+    });
+}

@@ -19,6 +19,8 @@ BIDA_ERR_DISTRIBUTION = 4
 BIDA_ERR_STATE = 5
 BIDA_ERR_CAPACITY = 6
 
+PDB_OFF, PDB_MIN, PDB_REPLACE = 0, 1, 2
+
 MODEL_LINEAR = 1
 MODEL_MLP = 2
 
@@ -53,6 +55,8 @@ EXPORTS = [
     "bida_gpu_evaluate_logits",
     "bida_gpu_evaluate_device",
     "bida_gpu_stream_status",
+    "bida_gpu_attach_pdb",
+    "bida_gpu_attach_pdb_file",
     "bida_gpu_info",
     "bida_gpu_debug_trace",
     "bida_gpu_trace_slots",
@@ -90,6 +94,8 @@ def lib() -> C.CDLL:
     L.bida_gpu_evaluate_logits.argtypes = [H, vp, i64, vp, vp]
     L.bida_gpu_evaluate_device.argtypes = [H, vp, i64, vp, vp, vp]
     L.bida_gpu_stream_status.argtypes = [H]
+    L.bida_gpu_attach_pdb.argtypes = [H, vp, i32, vp, C.c_uint64, i32]
+    L.bida_gpu_attach_pdb_file.argtypes = [H, C.c_char_p, i32]
     L.bida_gpu_info.argtypes = [H, C.POINTER(ModelInfo)]
     L.bida_gpu_debug_trace.argtypes = [H, vp]
     L.bida_gpu_launch_count.argtypes = [H]

@@ -98,6 +98,21 @@ class _GpuBackendBase:
                                                    C.c_void_p(stream))
         )
 
+    def attach_pdb(self, pattern, entries=None, mode: str = "min", path: str | None = None) -> None:
+        """PDB correction in the readout: h = min(h_model, h_PDB) ("min") or
+        h_PDB with the model still evaluated ("replace", PAPER.md:407 Table-1
+        mode); "off" detaches.  `entries` as PdbTable::entries() (pdb.hpp), or a
+        BPDB1 file via `path`."""
+        m = {"off": _native.PDB_OFF, "min": _native.PDB_MIN, "replace": _native.PDB_REPLACE}[mode]
+        L = _native.lib()
+        if path is not None:
+            _native.check(L.bida_gpu_attach_pdb_file(self._h, str(path).encode(), m))
+            return
+        pat = np.ascontiguousarray(pattern if pattern is not None else [], np.uint8)
+        ent = np.ascontiguousarray(entries if entries is not None else [], np.uint8)
+        _native.check(L.bida_gpu_attach_pdb(self._h, pat.ctypes.data_as(C.c_void_p), len(pat),
+                                            ent.ctypes.data_as(C.c_void_p), len(ent), m))
+
     def status(self) -> None:
         _native.check(_native.lib().bida_gpu_stream_status(self._h))
 

@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "linear.cuh"
 #include "mlp.cuh"
+#include "pdb.cuh"
 
 using namespace bida_gpu;
 
@@ -89,6 +90,9 @@ struct bida_gpu_evaluator {
     void *zc_in = nullptr, *zc_in_dev = nullptr;
     int32_t *zc_out = nullptr, *zc_out_dev = nullptr;
     std::atomic<int64_t> zc_calls{0};
+    // PDB correction (bida_gpu_attach_pdb)
+    uint8_t *d_pdb = nullptr;
+    PdbArgs pdb{};
     std::atomic<int64_t> launches{0};
 };
 
@@ -133,7 +137,7 @@ int launch(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h
         return BIDA_OK;
     if (ev->kind == BIDA_MODEL_MLP)
         return mlp_launch(ev->mlp, ev->domain, d_packed, n, d_h, d_logits, ev->err_dev, st,
-                          &ev->launches)
+                          &ev->launches, ev->d_pdb ? &ev->pdb : nullptr)
                    ? fail(BIDA_ERR_CUDA, mlp_last_error())
                    : BIDA_OK;
     LinearArgs a;
@@ -151,6 +155,9 @@ int launch(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h
     a.w_in_smem = ev->w_in_smem;
     a.any_rowflag = ev->any_rowflag;
     a.err = ev->err_dev;
+    a.pdb = ev->pdb;
+    if (!ev->d_pdb)
+        a.pdb.entries = nullptr;
     switch (ev->domain) {
     case BIDA_DOMAIN_STP2: return launch_linear_d<kSTP2>(ev, a, st);
     case BIDA_DOMAIN_STP3: return launch_linear_d<kSTP3>(ev, a, st);
@@ -241,6 +248,7 @@ void release(bida_gpu_evaluator *ev) {
     if (ev->zc_out) cudaFreeHost(ev->zc_out);
     if (ev->d_Wt) cudaFree(ev->d_Wt);
     if (ev->d_rowflag) cudaFree(ev->d_rowflag);
+    if (ev->d_pdb) cudaFree(ev->d_pdb);
     if (ev->mlp) mlp_destroy(ev->mlp);
     delete ev;
 }
@@ -622,6 +630,95 @@ int bida_gpu_info(const bida_gpu_evaluator *ev, bida_gpu_model_info *out) {
     out->device = ev->device;
     out->weights_in_smem = ev->w_in_smem;
     return BIDA_OK;
+}
+
+int bida_gpu_attach_pdb(bida_gpu_evaluator *ev, const uint8_t *pattern, int pattern_len,
+                        const uint8_t *entries, uint64_t n_entries, int mode) {
+    if (!ev)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL evaluator");
+    std::lock_guard<std::mutex> lk(ev->mu);
+    CUDA_TRY(cudaSetDevice(ev->device));
+    if (mode == BIDA_PDB_OFF) {
+        if (ev->d_pdb)
+            cudaFree(ev->d_pdb);
+        ev->d_pdb = nullptr;
+        ev->pdb = PdbArgs{};
+        return BIDA_OK;
+    }
+    if (mode != BIDA_PDB_MIN && mode != BIDA_PDB_REPLACE)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "unknown PDB mode");
+    if (!pattern || pattern_len <= 0 || pattern_len > kPdbMaxPattern || !entries)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "PDB pattern must have 1..8 labels");
+    const int n = ev->domain == BIDA_DOMAIN_RC ? 8 : ev->domain * ev->domain;
+    for (int i = 0; i < pattern_len; ++i) {
+        if (pattern[i] >= n)
+            return fail(BIDA_ERR_INVALID_ARGUMENT, ev->domain == BIDA_DOMAIN_RC
+                                                       ? "RubiksCube::Abstraction: only corner labels 0..7 supported"
+                                                       : "TilePuzzle::Abstraction: label out of range");
+        for (int j = 0; j < i; ++j)
+            if (pattern[j] == pattern[i])
+                return fail(BIDA_ERR_INVALID_ARGUMENT, "PDB pattern repeats a label");
+    }
+    // Abstraction::size (stp.hpp:204-206, rubiks.hpp:240-245)
+    uint64_t expect = 1;
+    for (int i = 0; i < pattern_len; ++i)
+        expect *= static_cast<uint64_t>(n - i);
+    if (ev->domain == BIDA_DOMAIN_RC)
+        for (int i = 0; i < pattern_len; ++i)
+            expect *= 3;
+    if (n_entries != expect)
+        return fail(BIDA_ERR_RUNTIME, "PDB entry count does not match pattern");
+    PdbArgs a{};
+    a.n = n_entries;
+    a.m = pattern_len;
+    a.mode = mode;
+    for (int i = 0; i < pattern_len; ++i) {
+        a.pat[i] = pattern[i];
+        unsigned long long w = 1;  // partial_perm_rank weight (ranking.hpp:43-45)
+        for (int k = 0; k < pattern_len - i - 1; ++k)
+            w *= static_cast<unsigned long long>(n - i - 1 - k);
+        a.w[i] = w;
+    }
+    uint8_t *d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, n_entries));
+    const cudaError_t e = cudaMemcpy(d, entries, n_entries, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return fail(BIDA_ERR_CUDA, std::string("PDB upload: ") + cudaGetErrorString(e));
+    }
+    if (ev->d_pdb)
+        cudaFree(ev->d_pdb);
+    ev->d_pdb = d;
+    a.entries = d;
+    ev->pdb = a;
+    return BIDA_OK;
+}
+
+int bida_gpu_attach_pdb_file(bida_gpu_evaluator *ev, const char *path, int mode) {
+    // BPDB1 (pdb.hpp:78-138): "BPDB1", tag ('S' / 'R'), board (N*N / 0), u8 plen,
+    // pattern, u64 entry count (little-endian), entries.
+    if (!ev)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL evaluator");
+    std::vector<unsigned char> b;
+    if (!path || !read_file(path, b))
+        return fail(BIDA_ERR_RUNTIME, std::string("cannot open PDB file: ") + (path ? path : ""));
+    if (b.size() < 5 || std::memcmp(b.data(), "BPDB1", 5) != 0)
+        return fail(BIDA_ERR_RUNTIME, std::string("not a BPDB1 file: ") + path);
+    if (b.size() < 8)
+        return fail(BIDA_ERR_RUNTIME, std::string("corrupt PDB header: ") + path);
+    const bool rc = ev->domain == BIDA_DOMAIN_RC;
+    const int tag = b[5], board = b[6], plen = b[7];
+    if (tag != (rc ? 'R' : 'S') || board != (rc ? 0 : ev->domain * ev->domain))
+        return fail(BIDA_ERR_RUNTIME, std::string("PDB domain mismatch: ") + path);
+    if (plen <= 0 || b.size() < 8 + static_cast<size_t>(plen) + 8)
+        return fail(BIDA_ERR_RUNTIME, std::string("corrupt PDB header: ") + path);
+    uint64_t cnt = 0;
+    for (int i = 0; i < 8; ++i)
+        cnt |= static_cast<uint64_t>(b[8 + plen + i]) << (8 * i);
+    const size_t off = 8 + plen + 8;
+    if (b.size() < off + cnt)
+        return fail(BIDA_ERR_RUNTIME, std::string("truncated PDB file: ") + path);
+    return bida_gpu_attach_pdb(ev, b.data() + 8, plen, b.data() + off, cnt, mode);
 }
 
 int bida_gpu_debug_trace(bida_gpu_evaluator *ev, long long *dev_buf) {

@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "encode.cuh"
+#include "pdb.cuh"
 #include "readout.cuh"
 
 namespace bida_gpu {
@@ -36,6 +37,7 @@ struct LinearArgs {
     int w_in_smem;           // Wt copied to shared memory by every CTA
     int any_rowflag;
     int *err;                // mapped host error words
+    PdbArgs pdb;             // optional PDB correction (pdb.cuh)
 };
 
 constexpr int kLinearThreads = 256;
@@ -89,6 +91,8 @@ linear_eval_kernel(const LinearArgs a) {
         }
         const int cnt = (a.n - base) < 32 ? static_cast<int>(a.n - base) : 32;
         int hres = 0;
+        // PDB entry of this lane's own state, fetched before the warp walks the 32 states
+        const int hpdb = (a.pdb.entries && me < a.n) ? pdb_fetch<DOMAIN>(a.pdb, mlo) : 0;
         for (int k = 0; k < cnt; ++k) {
             const uint64_t lo = __shfl_sync(kFull, mlo, k);
             const uint64_t hi = (T::PB == 16) ? __shfl_sync(kFull, mhi, k) : 0ull;
@@ -137,8 +141,17 @@ linear_eval_kernel(const LinearArgs a) {
                 hres = hmin;
             __syncwarp();
         }
-        if (me < a.n)
+        if (me < a.n) {
+            if (a.pdb.entries) {
+                if (hpdb < 0) {
+                    raise_error(a.err, kErrState);
+                    hres = 0;
+                } else {
+                    hres = pdb_combine(a.pdb, hres, hpdb);
+                }
+            }
             a.h_out[me] = hres;
+        }
     }
 }
 

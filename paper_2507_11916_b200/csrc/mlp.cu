@@ -33,6 +33,7 @@
 #include "common.cuh"
 #include "encode.cuh"
 #include "mlp.cuh"
+#include "pdb.cuh"
 #include "sm100.cuh"
 
 namespace bida_gpu {
@@ -76,6 +77,7 @@ struct MlpParams {
     double *logits_out;
     int *err;
     long long *trace;   // optional debug timeline (CTA 0): [warp][kTraceSlots] (clock64, tag)
+    PdbArgs pdb;        // optional PDB correction (pdb.cuh)
 };
 
 constexpr int kTraceSlots = 256;
@@ -445,6 +447,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             const uint64_t lo = nlo, hi = nhi;
             load_state(k + kstep, nlo, nhi);
             const bool bad = valid && state_bad(lo, hi);
+            // PDB entry prefetched at tile start; consumed when h is written
+            const int hpdb = (p.pdb.entries && reader && valid) ? pdb_fetch<DOMAIN>(p.pdb, lo) : 0;
             if (bad && reader)
                 raise_error(p.err, kErrState);
             const bool live = valid && !bad;
@@ -573,7 +577,16 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             if (reader && valid) {
                 if (dist_bad)
                     raise_error(p.err, kErrDistribution);
-                p.h_out[st] = (live && !dist_bad) ? hmin : 0;
+                int h = (live && !dist_bad) ? hmin : 0;
+                if (p.pdb.entries && live) {
+                    if (hpdb < 0) {
+                        raise_error(p.err, kErrState);
+                        h = 0;
+                    } else {
+                        h = pdb_combine(p.pdb, h, hpdb);
+                    }
+                }
+                p.h_out[st] = h;
             }
         }
     }
@@ -871,8 +884,12 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
 }
 
 int mlp_launch(MlpModel *m, int domain, const void *d_packed, int64_t n, int32_t *d_h, double *d_logits,
-               int *err_dev, cudaStream_t st, std::atomic<int64_t> *launches) {
+               int *err_dev, cudaStream_t st, std::atomic<int64_t> *launches, const PdbArgs *pdb) {
     MlpParams p = m->p;  // per-call copy: concurrent launches on one handle are safe
+    if (pdb)
+        p.pdb = *pdb;
+    else
+        p.pdb.entries = nullptr;
     p.trace = m->trace;
     p.packed = d_packed;
     p.n = n;

@@ -39,6 +39,7 @@ struct Args {
     int gpus = 1;
     bool immediate = false;  // AIDA*: evaluate inline on the searcher threads
     int table1_corners = 0;  // >0: "Table-1" mode with an N-corner PDB (Rubik's)
+    bool gpu_pdb = false;    // Table-1 on the GPU: PDB lookup fused into the device readout
 };
 
 // Table-1 mode: the network is evaluated for
@@ -63,13 +64,17 @@ private:
     std::shared_ptr<const Heuristic<D>> pdb_;
 };
 
+inline std::string corner_pdb_path(int corners) {
+    return "/tmp/bida_rc_corner" + std::to_string(corners) + ".pdb";
+}
+
 template <class D>
 std::shared_ptr<const Heuristic<D>> corner_pdb(int corners) {
     if constexpr (std::is_same_v<D, RubiksCube>) {
         std::vector<std::uint8_t> pat;
         for (int c = 0; c < corners; ++c)
             pat.push_back(static_cast<std::uint8_t>(c));
-        const std::string cache = "/tmp/bida_rc_corner" + std::to_string(corners) + ".pdb";
+        const std::string cache = corner_pdb_path(corners);
         std::shared_ptr<const PdbTable<D>> t;
         try {
             t = std::make_shared<const PdbTable<D>>(PdbTable<D>::load(cache));
@@ -127,6 +132,15 @@ std::vector<std::unique_ptr<EvaluatorBackend<D>>> make_mode_backends(const Args 
     if (mode == "pdb") {
         for (int e = 0; e < a.evaluators; ++e)
             v.push_back(std::make_unique<Table1Backend<D>>(nullptr, pdb));
+        return v;
+    }
+    if (mode == "gpu" && a.gpu_pdb) {
+        // the network and the PDB lookup both run in the device readout
+        for (auto &b : make_backends<D>(a, true)) {
+            static_cast<bida_gpu::GpuBackend<D> *>(b.get())->attach_pdb_file(corner_pdb_path(a.table1_corners),
+                                                                             BIDA_PDB_REPLACE);
+            v.push_back(std::move(b));
+        }
         return v;
     }
     for (auto &b : make_backends<D>(a, mode == "gpu"))
@@ -223,7 +237,8 @@ int run(const Args &a) {
             js << "], \"threads\": " << a.threads << ", \"work_num\": " << a.work_num << ", \"batch\": " << a.batch
                << ", \"timeout_us\": " << a.timeout_us << ", \"evaluators\": " << a.evaluators
                << ", \"immediate\": " << (a.immediate ? "true" : "false")
-               << ", \"table1_corners\": " << a.table1_corners << "}";
+               << ", \"table1_corners\": " << a.table1_corners << ", \"gpu_pdb\": " << (a.gpu_pdb ? "true" : "false")
+               << "}";
             std::printf("%s\n", js.str().c_str());
             std::fflush(stdout);
         }
@@ -266,6 +281,7 @@ int main(int argc, char **argv) {
         else if (k == "--count") a.count = std::stoi(val());
         else if (k == "--immediate") a.immediate = true;
         else if (k == "--table1-pdb") a.table1_corners = std::stoi(val());
+        else if (k == "--gpu-pdb") a.gpu_pdb = true;
         else {
             std::fprintf(stderr, "unknown flag %s\n", k.c_str());
             return 2;

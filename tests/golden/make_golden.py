@@ -59,6 +59,19 @@ def main() -> None:
                         h=h, manhattan=md, n_korf=len(korf))
     print("manhattan_stp4", len(packed))
 
+    # Pattern databases built by the reference (PdbTable<D>::build, pdb.hpp:30-64)
+    # and its lookups (pdb.hpp:66-69) on reference walks.
+    for name, d, pat, lmax in [("pdb_rc_c4", RC, [0, 1, 2, 3], 30), ("pdb_stp3_p5", STP3, [1, 2, 3, 4, 5], 40),
+                               ("pdb_stp4_p4", STP4, [1, 2, 3, 4], 60)]:
+        entries = ref.pdb_build(d, pat)
+        packed = ref.random_walks(d, 2000, 0, lmax, 4242)
+        path = "/tmp/_golden.pdb"
+        ref.pdb_build_save(d, pat, path)
+        h = ref.pdb_lookup_file(d, path, packed)
+        np.savez_compressed(os.path.join(HERE, name + ".npz"), domain=d, pattern=np.array(pat, np.uint8),
+                            entries=entries, packed=packed, h=h)
+        print(name, len(entries), np.bincount(h))
+
     stp8 = ref.load_instances(STP3, os.path.join(DATA, "stp8_100.txt"))
     rc50 = ref.load_instances(RC, os.path.join(DATA, "rc50.txt"))
     np.savez_compressed(os.path.join(HERE, "instances.npz"), korf10=korf, stp8_100=stp8, rc50=rc50)

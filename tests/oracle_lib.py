@@ -59,6 +59,7 @@ class Oracle:
         L.orc_active_indices.argtypes = [C.c_int, _p, _p]
         L.orc_mlp_evaluate_blob.argtypes = [_p, C.c_size_t, C.c_int, C.c_double, _p, _i64, _p, _p, C.c_int]
         L.orc_manhattan.argtypes = [C.c_int, _p, _i64, _p]
+        L.orc_pdb_lookup.argtypes = [C.c_int, _p, C.c_int, _p, C.c_uint64, _p, _i64, _p]
         L.orc_blin1_parse.argtypes = [_p, C.c_size_t, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.POINTER(C.c_float))]
         self.L = L
 
@@ -104,6 +105,15 @@ class Oracle:
         assert self.L.orc_manhattan(domain, _ptr(packed), len(packed), _ptr(out)) == 0
         return out
 
+    def pdb_lookup(self, domain, pattern, entries, packed):
+        pat = np.ascontiguousarray(pattern, np.uint8)
+        ent = np.ascontiguousarray(entries, np.uint8)
+        out = np.zeros(len(packed), np.int32)
+        rc = self.L.orc_pdb_lookup(domain, _ptr(pat), len(pat), _ptr(ent), len(ent), _ptr(packed), len(packed), _ptr(out))
+        if rc:
+            raise ValueError("invalid state for the pattern")
+        return out
+
 
 class RefLib:
     """The reference implementation itself (header-only C++ compiled unchanged)."""
@@ -127,6 +137,9 @@ class RefLib:
         L.ref_quantile_class.argtypes = [_p, C.c_int, C.c_double, C.POINTER(C.c_int)]
         L.ref_ensemble_min.argtypes = [_p, C.c_int, C.POINTER(C.c_int)]
         L.ref_manhattan.argtypes = [C.c_int, _p, _i64, _p]
+        L.ref_pdb_build.argtypes = [C.c_int, _p, C.c_int, _p, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.ref_pdb_lookup_file.argtypes = [C.c_int, C.c_char_p, _p, _i64, _p]
+        L.ref_pdb_build_save.argtypes = [C.c_int, _p, C.c_int, C.c_char_p]
         L.ref_load_instances.argtypes = [C.c_int, C.c_char_p, _p, _i64, C.POINTER(_i64)]
         self.L = L
 
@@ -182,6 +195,24 @@ class RefLib:
     def manhattan(self, domain, packed):
         out = np.zeros(len(packed), np.int32)
         self._check(self.L.ref_manhattan(domain, _ptr(packed), len(packed), _ptr(out)))
+        return out
+
+    def pdb_build(self, domain, pattern, cap=1 << 26):
+        """PdbTable<D>::build (pdb.hpp:30-64) -> entries (uint8)."""
+        pat = np.ascontiguousarray(pattern, np.uint8)
+        buf = np.zeros(cap, np.uint8)
+        n = C.c_uint64(0)
+        self._check(self.L.ref_pdb_build(domain, _ptr(pat), len(pat), _ptr(buf), cap, C.byref(n)))
+        return buf[: n.value].copy()
+
+    def pdb_build_save(self, domain, pattern, path):
+        pat = np.ascontiguousarray(pattern, np.uint8)
+        self._check(self.L.ref_pdb_build_save(domain, _ptr(pat), len(pat), path.encode()))
+
+    def pdb_lookup_file(self, domain, path, packed):
+        """PdbTable<D>::load + lookup (pdb.hpp:66-69, 98-138)."""
+        out = np.zeros(len(packed), np.int32)
+        self._check(self.L.ref_pdb_lookup_file(domain, path.encode(), _ptr(packed), len(packed), _ptr(out)))
         return out
 
     def load_instances(self, domain, path, cap=100000):

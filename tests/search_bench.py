@@ -86,14 +86,19 @@ def rc_bench(a):
     n = a.threads
     tl = str(a.time_limit)
     runs = [
-        ("gpu batch_idastar nn+pdb E=1", "gpu", ["--evaluators", "1", "--work-num", "64", "--batch", "16384", "--timeout-us", "200"]),
-        ("gpu batch_idastar nn+pdb E=2", "gpu", ["--evaluators", "2", "--work-num", "64", "--batch", "8192", "--timeout-us", "200"]),
+        ("gpu batch_idastar nn+gpu-pdb E=1", "gpu", ["--gpu-pdb", "--evaluators", "1", "--work-num", "64", "--batch", "16384", "--timeout-us", "200"]),
+        ("gpu batch_idastar nn+gpu-pdb E=2", "gpu", ["--gpu-pdb", "--evaluators", "2", "--work-num", "64", "--batch", "8192", "--timeout-us", "200"]),
+        ("gpu batch_idastar nn+gpu-pdb E=4", "gpu", ["--gpu-pdb", "--evaluators", "4", "--work-num", "64", "--batch", "8192", "--timeout-us", "200"]),
+        ("gpu batch_idastar nn+cpu-pdb E=2", "gpu", ["--evaluators", "2", "--work-num", "64", "--batch", "8192", "--timeout-us", "200"]),
         ("cpu batch_idastar nn+pdb E=n", "cpu", ["--evaluators", str(n), "--work-num", "8", "--batch", "512", "--timeout-us", "200"]),
         ("cpu aidastar nn+pdb (immediate)", "cpu", ["--immediate", "--evaluators", "1", "--work-num", "1", "--batch", "1"]),
         ("cpu aidastar pdb only (no nn)", "pdb", ["--immediate", "--evaluators", "1", "--work-num", "1", "--batch", "1"]),
     ]
     lines = []
+    only = os.environ.get("BIDA_SEARCH_ONLY")  # e.g. "gpu" to rerun just the GPU rows
     for label, mode, extra in runs:
+        if only and not label.startswith(only):
+            continue
         cmd = [BIN, "--domain", "rc", "--walks", a.walks, "--model", "mlp:" + model, "--mode", mode,
                "--table1-pdb", "5", "--threads", str(n), "--time-limit", tl, *extra]
         out = subprocess.run(cmd, capture_output=True, text=True, timeout=3600)

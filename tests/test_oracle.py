@@ -161,3 +161,11 @@ def test_package_walks_are_valid_states(orc):
         assert (x.sum(1) == {STP2: 4, STP3: 9, STP4: 16, RC: 20}[d]).all()
         if HAVE_REF:
             assert (RefLib().repack(d, packed) == packed).all()
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "pdb_*.npz"))))
+def test_pdb_rank_lookup_matches_reference_golden(orc, path):
+    """orc_pdb_rank/lookup restate Abstraction::rank_state + PdbTable::lookup."""
+    g = np.load(path)
+    h = orc.pdb_lookup(int(g["domain"]), g["pattern"], g["entries"], g["packed"])
+    assert (h == g["h"]).all()
