@@ -110,3 +110,21 @@ def test_rc_mlp_search_matches_oracle_backend(tmp_path):
                 "--threads", "4", "--work-num", "4", "--batch", "1024", "--timeout-us", "200",
                 "--time-limit", "120"])
     compare(rows)
+
+
+def test_rc_table1_gpu_pdb_matches_cpu(tmp_path):
+    """Table-1 mode: network evaluated, search guided by a corner
+    PDB.  GPU: network + PDB lookup in the device readout (--gpu-pdb); CPU: the
+    oracle network + the reference's PdbTable::lookup.  Admissible h -> optimal
+    costs, identical trees."""
+    from paper_2507_11916_b200.models import make_bmlp1
+
+    blob = make_bmlp1("rc", hidden=[128, 128], classes=21, ensemble=1, seed=11)
+    path = tmp_path / "m.bmlp"
+    path.write_bytes(blob)
+    rows = run(["--domain", "rc", "--walks", "4:6:8:5", "--model", "mlp:" + str(path), "--table1-pdb", "4",
+                "--gpu-pdb", "--threads", "4", "--work-num", "4", "--batch", "1024", "--timeout-us", "200",
+                "--time-limit", "300"])
+    by = compare(rows)
+    for i, m in by.items():
+        assert m["gpu"]["cost"] <= 8
