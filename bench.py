@@ -317,6 +317,47 @@ def cpu_rate(wl, seconds_target, threads, seed=7):
     return run, kind, n * reps
 
 
+SEARCH_WALKS = "1:15:15:2508"  # one walk-15 Rubik's scramble (configs[1]: walks 14-16)
+
+
+def search_leg(wl, seconds, threads, cpu: bool):
+    """Batch IDA* nodes/s (BASELINE metric, second half): the reference's own
+    batch_idastar (search.hpp:101-237) over a walk-15 Rubik's scramble, the
+    workload's BMLP1 network evaluated for every generated node, search guided
+    by the reference's 5-corner PDB (PAPER.md:407 Table-1 mode).
+    GPU: tools/bin/bida_search with 8 GpuBackend evaluators (network + PDB in
+    the device readout).  CPU (cpu=True, baseline leg only): the test build
+    tests/cpp/bin/search_parity with the oracle's CPU network, one evaluator
+    per searcher thread."""
+    from paper_2507_11916_b200.models import make_bmlp1
+
+    if wl["domain"] != "rc" or wl["kind"] != "mlp":
+        return None
+    model = f"/tmp/bida_bench_{os.getpid()}.bmlp"
+    with open(model, "wb") as f:
+        f.write(make_bmlp1("rc", hidden=wl["H"], classes=wl["C"], ensemble=wl["E"], seed=2507))
+    if cpu:
+        exe = os.path.join(ROOT, "tests", "cpp", "bin", "search_parity")
+        extra = ["--mode", "cpu", "--evaluators", str(threads), "--work-num", "8", "--batch", "512", "--timeout-us", "200"]
+    else:
+        exe = os.path.join(ROOT, "tools", "bin", "bida_search")
+        extra = ["--mode", "gpu", "--gpu-pdb", "--evaluators", "8", "--work-num", "128", "--batch", "16384",
+                 "--timeout-us", "25"]
+    if not os.path.exists(exe):
+        return {"unavailable": f"{exe} not built"}
+    cmd = [exe, "--domain", "rc", "--walks", SEARCH_WALKS, "--model", "mlp:" + model, "--q", str(wl["q"]),
+           "--table1-pdb", "5", "--threads", str(threads), "--time-limit", str(seconds), *extra]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    os.unlink(model)
+    rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    if out.returncode or not rows:
+        return {"unavailable": (out.stderr or "no output").strip().splitlines()[-1][:200]}
+    r = rows[0]
+    return {"value": r["nodes_per_s"], "unit": "nodes/s", "evals_per_s": r["evals_per_s"],
+            "generated": r["generated"], "wall_s": r["wall_s"], "status": r["status"], "mean_batch": r["mean_batch"],
+            "threads": threads, "evaluators": r["evaluators"], "work_num": r["work_num"], "timeout_us": r["timeout_us"]}
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -362,6 +403,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample size (seconds of work)")
     ap.add_argument("--ref-step-seconds", type=float, default=2.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--search-seconds", type=float, default=10.0,
+                    help="Batch IDA* nodes/s leg (RC MLP workloads, N=1); 0 disables")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = WORKLOADS[args.workload]
@@ -448,6 +491,21 @@ def main():
             "value": n / dt, "unit": "evals/s", "cores": threads, "kind": kind,
             "sample": f"{n} packed {wl['domain']} random-walk states (lengths 0-30), one call, {dt:.1f} s",
         }
+    if world == 1 and args.search_seconds > 0:
+        threads = host_cores()
+        sr = search_leg(wl, args.search_seconds, threads, cpu=False)
+        if sr is not None:
+            sr = {"metric": "batch_idastar_nodes_per_s", **sr,
+                  "config": {"domain": "rc", "instance": "random walk of 15 moves (seed 2508)", "heuristic":
+                             "BMLP1 evaluated per node + 5-corner PDB guidance (PAPER.md:407 Table-1 mode)",
+                             "search": "reference batch_idastar (search.hpp:101-237), unchanged"}}
+            if not args.no_cpu_baseline and "value" in sr:
+                cb = search_leg(wl, args.search_seconds, threads, cpu=True)
+                if cb and "value" in cb:
+                    sr["cpu_baseline"] = {"value": cb["value"], "unit": "nodes/s", "cores": threads, "kind": "port",
+                                          "sample": f"{cb['wall_s']:.0f} s of the same search, oracle BMLP1 on "
+                                                    f"{threads} CPU evaluator threads"}
+            line["search"] = sr
     print(json.dumps(line), flush=True)
 
 

@@ -1,12 +1,14 @@
-// search_parity.cpp — runs the reference's own Batch IDA* (search.hpp:101-237)
-// with (a) the reference CPU evaluator and (b) the B200 GpuBackend dropped in
-// through bida::EvaluatorBackend, on the same instances and weights, and
-// prints one JSON line per (instance, backend): cost, status, threshold
-// history, per-iteration counts, nodes/s, evals/s.
-//
-// Built against the reference headers (reference search kept as-is, north
-// star) + include/bida_gpu_backend.hpp + libbida_gpu.so.  For BMLP1 models
-// the CPU side is the oracle's C restatement (the reference has no MLP).
+// bida_search.cpp — the builder's search driver: the reference's own Batch
+// IDA* / AIDA* (search.hpp:101-247, unchanged) with evaluators chosen per run:
+//   gpu : bida_gpu::GpuBackend<D> (include/bida_gpu_backend.hpp) per evaluator
+//   cpu : the reference's LinearModelBackend (BLIN1); BMLP1 on the CPU only in
+//         the test build (-DBIDA_WITH_ORACLE, tests/cpp/bin/search_parity),
+//         where the oracle's C restatement stands in (the reference has no MLP)
+//   pdb : the reference's PdbTable lookups only (AIDA* baseline)
+// It prints one JSON line per (instance, backend): cost, status, threshold
+// history, per-iteration counts, nodes/s, evals/s.  tools/bin/bida_search is
+// the product build (no oracle linked); tests/test_gpu_search.py drives the
+// test build to check GPU and CPU searches agree.
 //
 //   search_parity --domain stp4 --instances korf10.txt --model linear:w.blin --q 0.5 \
 //                 --threads 8 --work-num 16 --batch 4096 --timeout-us 200 --evaluators 1 --mode both
@@ -23,7 +25,9 @@
 
 #include "bida/search.hpp"
 #include "bida_gpu_backend.hpp"
-#include "../../oracle/bida_oracle.h"
+#ifdef BIDA_WITH_ORACLE
+#include "../oracle/bida_oracle.h"
+#endif
 
 using namespace bida;
 
@@ -96,6 +100,7 @@ std::vector<unsigned char> read_all(const std::string &p) {
     return std::vector<unsigned char>(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
 }
 
+#ifdef BIDA_WITH_ORACLE
 // CPU BMLP1 backend over the oracle restatement (test infrastructure).
 template <class D>
 class OracleMlpBackend final : public EvaluatorBackend<D> {
@@ -119,6 +124,7 @@ private:
     orc_mlp m_{};
     double q_;
 };
+#endif
 
 template <class D>
 std::vector<std::unique_ptr<EvaluatorBackend<D>>> make_backends(const Args &a, bool gpu);
@@ -164,7 +170,11 @@ std::vector<std::unique_ptr<EvaluatorBackend<D>>> make_backends(const Args &a, b
             if (gpu)
                 v.push_back(bida_gpu::GpuBackend<D>::load_mlp(dev, path, a.q));
             else
+#ifdef BIDA_WITH_ORACLE
                 v.push_back(std::make_unique<OracleMlpBackend<D>>(path, a.q));
+#else
+                throw std::runtime_error("BMLP1 on the CPU needs the test build (tests/cpp/bin/search_parity)");
+#endif
         } else {
             throw std::runtime_error("model must be linear:PATH or mlp:PATH");
         }
