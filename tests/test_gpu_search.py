@@ -128,3 +128,18 @@ def test_rc_table1_gpu_pdb_matches_cpu(tmp_path):
     by = compare(rows)
     for i, m in by.items():
         assert m["gpu"]["cost"] <= 8
+
+
+def test_batch_astar_with_gpu_evaluator(tmp_path, manhattan_blins):
+    """Batch A* (search.hpp:350-503) through the same boundary: GPU and CPU
+    evaluators give the same optimal costs on the 8-puzzle instances."""
+    g = np.load(os.path.join(GOLDEN, "instances.npz"))
+    inst = write_instances(tmp_path, "stp8.txt", g["stp8_100"], "stp3")
+    rows = run(["--domain", "stp3", "--instances", inst, "--model", "linear:" + manhattan_blins[0],
+                "--algo", "batch-astar", "--batch", "64", "--timeout-us", "100", "--count", "25"])
+    by = {}
+    for r in rows:
+        by.setdefault(r["instance"], {})[r["mode"]] = r
+    for i, m in by.items():
+        assert m["gpu"]["status"] == m["cpu"]["status"] == "solved"
+        assert m["gpu"]["cost"] == m["cpu"]["cost"]

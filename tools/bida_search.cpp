@@ -44,6 +44,7 @@ struct Args {
     bool immediate = false;  // AIDA*: evaluate inline on the searcher threads
     int table1_corners = 0;  // >0: "Table-1" mode with an N-corner PDB (Rubik's)
     bool gpu_pdb = false;    // Table-1 on the GPU: PDB lookup fused into the device readout
+    std::string algo = "batch-idastar";  // or "batch-astar" (search.hpp:350-503)
 };
 
 // Table-1 mode: the network is evaluated for
@@ -225,7 +226,9 @@ int run(const Args &a) {
     for (const std::string &mode : modes) {
         EvaluatorGroup<D> group(make_mode_backends<D>(a, mode), a.batch, a.timeout_us, a.immediate);
         for (int i = a.first; i < static_cast<int>(insts.size()) && i < a.first + a.count; ++i) {
-            const SearchResult<D> r = batch_idastar<D>(insts[static_cast<std::size_t>(i)], group, cfg);
+            const SearchResult<D> r = a.algo == "batch-astar"
+                                          ? batch_astar<D>(insts[static_cast<std::size_t>(i)], group, cfg)
+                                          : batch_idastar<D>(insts[static_cast<std::size_t>(i)], group, cfg);
             const SearchStats &s = r.stats;
             std::ostringstream js;
             js << "{\"instance\": " << i << ", \"mode\": \"" << mode << "\", \"status\": \"" << status_name(r.status)
@@ -248,7 +251,7 @@ int run(const Args &a) {
                << ", \"timeout_us\": " << a.timeout_us << ", \"evaluators\": " << a.evaluators
                << ", \"immediate\": " << (a.immediate ? "true" : "false")
                << ", \"table1_corners\": " << a.table1_corners << ", \"gpu_pdb\": " << (a.gpu_pdb ? "true" : "false")
-               << "}";
+               << ", \"algo\": \"" << a.algo << "\"}";
             std::printf("%s\n", js.str().c_str());
             std::fflush(stdout);
         }
@@ -292,6 +295,7 @@ int main(int argc, char **argv) {
         else if (k == "--immediate") a.immediate = true;
         else if (k == "--table1-pdb") a.table1_corners = std::stoi(val());
         else if (k == "--gpu-pdb") a.gpu_pdb = true;
+        else if (k == "--algo") a.algo = val();
         else {
             std::fprintf(stderr, "unknown flag %s\n", k.c_str());
             return 2;
