@@ -135,6 +135,8 @@ def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("BIDA_BENCH_SINGLE_DEVICE") == "1":
+        local = 0  # plumbing test: every rank on cuda:0 (use BIDA_BENCH_BACKEND=gloo)
     if world > 1:
         import torch.distributed as dist
 

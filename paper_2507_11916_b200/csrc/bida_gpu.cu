@@ -57,6 +57,11 @@ int packed_bytes(int domain) {
 
 } // namespace
 
+// Host<->device pipelining of large batches: kSlots chunks of up to kMaxSlot
+// states in flight on kSlots streams, so the H2D copy of chunk i+1.. overlaps
+// the kernel of chunk i and the D2H of chunk i-1 (copy engines are full duplex).
+constexpr int kSlots = 4;
+
 struct bida_gpu_evaluator {
     int kind = 0, domain = 0, F = 0, C = 0, E = 0, device = 0;
     double q = 0.5, thr = 0.0;
@@ -77,13 +82,13 @@ struct bida_gpu_evaluator {
     int hidden[8] = {0};
 
     std::mutex mu;
-    cudaStream_t stream[2] = {nullptr, nullptr};
-    cudaEvent_t done[2] = {nullptr, nullptr};
+    cudaStream_t stream[kSlots] = {};
+    cudaEvent_t done[kSlots] = {};
     int64_t slot_cap = 0;
-    void *h_in[2] = {nullptr, nullptr};
-    int32_t *h_h[2] = {nullptr, nullptr};
-    void *d_in[2] = {nullptr, nullptr};
-    int32_t *d_h[2] = {nullptr, nullptr};
+    void *h_in[kSlots] = {};
+    int32_t *h_h[kSlots] = {};
+    void *d_in[kSlots] = {};
+    int32_t *d_h[kSlots] = {};
     int *err_host = nullptr; // mapped pinned, kErrWords ints
     int *err_dev = nullptr;
     // small-batch zero-copy path: mapped pinned in/out read/written by the kernel
@@ -98,7 +103,7 @@ struct bida_gpu_evaluator {
 
 namespace {
 
-constexpr int64_t kMaxSlot = int64_t(1) << 20;
+constexpr int64_t kMaxSlot = int64_t(1) << 18;
 // Batches up to this size skip the copy engines: the kernel reads the packed
 // states from mapped pinned memory and writes h straight back into it (one
 // launch + one stream sync per call; search batches are 1-8K states).
@@ -186,7 +191,7 @@ int ensure_slots(bida_gpu_evaluator *ev, int64_t n) {
     while (cap < want)
         cap <<= 1;
     const int pb = packed_bytes(ev->domain);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kSlots; ++s) {
         if (ev->h_in[s]) cudaFreeHost(ev->h_in[s]);
         if (ev->h_h[s]) cudaFreeHost(ev->h_h[s]);
         if (ev->d_in[s]) cudaFree(ev->d_in[s]);
@@ -215,7 +220,7 @@ int common_init(bida_gpu_evaluator *ev, int device) {
         return fail(BIDA_ERR_CUDA, std::string("this library is built for sm_100a (B200); device is ") +
                                        prop.name);
     ev->num_sms = prop.multiProcessorCount;
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kSlots; ++s) {
         CUDA_TRY(cudaStreamCreateWithFlags(&ev->stream[s], cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreateWithFlags(&ev->done[s], cudaEventDisableTiming));
     }
@@ -234,7 +239,7 @@ void release(bida_gpu_evaluator *ev) {
     if (!ev)
         return;
     cudaSetDevice(ev->device);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kSlots; ++s) {
         if (ev->stream[s]) cudaStreamSynchronize(ev->stream[s]);
         if (ev->h_in[s]) cudaFreeHost(ev->h_in[s]);
         if (ev->h_h[s]) cudaFreeHost(ev->h_h[s]);
@@ -523,7 +528,11 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
     // go through the handle's pinned staging slots.
     const bool in_pinned = is_pinned(packed);
     const bool out_pinned = is_pinned(h_out);
-    int64_t pend_off[2] = {-1, -1}, pend_n[2] = {0, 0};
+    int64_t pend_off[kSlots], pend_n[kSlots];
+    for (int k = 0; k < kSlots; ++k) {
+        pend_off[k] = -1;
+        pend_n[k] = 0;
+    }
     int rc = BIDA_OK;
     auto drain = [&](int s) -> int {
         if (pend_off[s] < 0)
@@ -537,7 +546,7 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         return BIDA_OK;
     };
     int slot = 0;
-    for (int64_t i0 = 0; i0 < n && rc == BIDA_OK; i0 += ev->slot_cap, slot ^= 1) {
+    for (int64_t i0 = 0; i0 < n && rc == BIDA_OK; i0 += ev->slot_cap, slot = (slot + 1) % kSlots) {
         const int64_t m = std::min<int64_t>(ev->slot_cap, n - i0);
         if ((rc = drain(slot)))
             break;
@@ -576,14 +585,14 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
             }
         }
     }
-    for (int s = 0; s < 2; ++s) {
-        const int r = drain(slot ^ s ^ 1) ? BIDA_ERR_CUDA : BIDA_OK;
+    for (int s = 0; s < kSlots; ++s) {  // oldest pending chunk first
+        const int r = drain((slot + s) % kSlots) ? BIDA_ERR_CUDA : BIDA_OK;
         if (rc == BIDA_OK)
             rc = r;
     }
     // make sure no stream still writes staging before we return
-    cudaStreamSynchronize(ev->stream[0]);
-    cudaStreamSynchronize(ev->stream[1]);
+    for (int s = 0; s < kSlots; ++s)
+        cudaStreamSynchronize(ev->stream[s]);
     if (d_logits)
         cudaFree(d_logits);
     if (rc != BIDA_OK) {

@@ -69,6 +69,68 @@ __global__ void __launch_bounds__(128, 1) bench(int n_mma, int N, int layout, lo
         sm100::tmem_dealloc(tmem, 512);
 }
 
+// SS MMAs (A and B from SMEM) issued by warp 0 while `sts_warps` other warps
+// stream st.shared.v4 into a separate SMEM region: does epilogue-style SMEM
+// traffic slow the tensor core's operand reads?  ts=1: A from TMEM instead.
+__global__ void __launch_bounds__(512, 1) contention(int n_mma, int N, int sts_warps, int ts, long long *out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    __shared__ volatile int stop;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        sm100::mbar_init(&bar, 1);
+        sm100::fence_barrier_init();
+        stop = 0;
+    }
+    for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+        reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+    sm100::fence_proxy_async_smem();
+    if (warp == 0)
+        sm100::tmem_alloc(&tslot, 512);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = tslot;
+    if (warp == 0) {
+        if (threadIdx.x == 0) {
+            const uint32_t sA = sm100::smem_u32(smem), sB = sA + 32 * 1024;
+            const uint32_t idesc = sm100::make_idesc_i8(N);
+            const long long t0 = clock64();
+            for (int i = 0; i < n_mma; ++i) {
+                const int ks = i & 3;
+                const uint64_t b = sm100::make_smem_desc(sB + ks * (N * 32u), N * 16u, 128u);
+                if (ts) {
+                    // A operand in TMEM columns [256 + 8ks, +8): 128 lanes x 32 int8
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+                        "r"(tmem + 256 + ks * 8), "l"(b), "r"(idesc), "r"(i > 0 ? 1u : 0u)
+                        : "memory");
+                } else {
+                    const uint64_t a = sm100::make_smem_desc(sA + ks * 4096u, 2048u, 128u);
+                    sm100::mma_i8(tmem, a, b, idesc, i > 0 ? 1u : 0u);
+                }
+            }
+            sm100::mma_commit(&bar);
+            sm100::mbar_wait(&bar, 0);
+            out[blockIdx.x] = clock64() - t0;
+            stop = 1;
+        }
+    } else if (warp <= sts_warps) {
+        const uint32_t base = sm100::smem_u32(smem) + 64 * 1024 + (warp - 1) * 512 + (threadIdx.x & 31) * 16;
+        while (!stop)
+            for (int r = 0; r < 16; ++r)
+                sm100::st_shared_v4(base, r, r, r, r);
+    }
+    __syncwarp();
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    if (warp == 0)
+        sm100::tmem_dealloc(tmem, 512);
+}
+
 int main() {
     long long *d_out, h_out[2 * 148];
     cudaMalloc(&d_out, sizeof(h_out));
@@ -97,5 +159,24 @@ int main() {
                        100.0 * floor_cyc / (total / n));
             }
         }
+    cudaFuncSetAttribute(contention, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    for (int ts = 0; ts < 2; ++ts)
+        for (int N : {128, 256})
+            for (int w : {0, 4, 8, 15}) {
+                const int n = 512;
+                contention<<<148, 512, 96 * 1024>>>(n, N, w, ts, d_out);
+                cudaError_t e = cudaDeviceSynchronize();
+                if (e != cudaSuccess) {
+                    printf("error %s\n", cudaGetErrorString(e));
+                    return 1;
+                }
+                cudaMemcpy(h_out, d_out, sizeof(long long) * 148, cudaMemcpyDeviceToHost);
+                double tot = 0;
+                for (int g = 0; g < 148; ++g)
+                    tot += h_out[g];
+                tot /= 148;
+                printf("contention A=%s N=%3d sts_warps=%2d  %.1f cyc/mma (floor %.0f)\n", ts ? "tmem" : "smem", N, w,
+                       tot / n, 128.0 * N / 256.0);
+            }
     return 0;
 }
