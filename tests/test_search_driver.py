@@ -1,0 +1,68 @@
+"""CPU: the search driver (tools/bida_search: the reference's batch_idastar /
+batch_astar with evaluators chosen per run) solves instances with the
+reference's own CPU evaluators, and refuses GPU-only configurations cleanly
+when no device is present.  The GPU legs are in test_gpu_search.py."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOOL = os.path.join(ROOT, "tools", "bin", "bida_search")
+DATA = "/root/reference/proj/data"
+
+pytestmark = pytest.mark.skipif(not os.path.exists(TOOL), reason="tools/bin/bida_search not built")
+
+
+def run(args):
+    out = subprocess.run([TOOL, *args], capture_output=True, text=True, timeout=300)
+    return out.returncode, [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")], out.stderr
+
+
+@pytest.fixture(scope="module")
+def man3(tmp_path_factory):
+    import sys
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import manhattan_linear_weights
+
+    import paper_2507_11916_b200 as bida
+
+    p = tmp_path_factory.mktemp("w") / "man3.blin"
+    p.write_bytes(bida.blin1_bytes("stp3", manhattan_linear_weights(3, 40, 4.0), 40))
+    return str(p)
+
+
+def test_cpu_linear_batch_idastar_and_astar_agree(tmp_path, man3):
+    g = np.load(os.path.join(ROOT, "tests", "golden", "instances.npz"))
+    inst = tmp_path / "stp8.txt"
+    inst.write_text("\n".join("stp 3 " + " ".join(str((int(v) >> (4 * c)) & 15) for c in range(9))
+                              for v in g["stp8_100"][:20]) + "\n")
+    rc, ida, err = run(["--domain", "stp3", "--instances", str(inst), "--model", "linear:" + man3, "--mode", "cpu",
+                        "--threads", "2", "--work-num", "2", "--batch", "32"])
+    assert rc == 0, err
+    rc, ast, err = run(["--domain", "stp3", "--instances", str(inst), "--model", "linear:" + man3, "--mode", "cpu",
+                        "--algo", "batch-astar", "--batch", "32"])
+    assert rc == 0, err
+    assert len(ida) == len(ast) == 20
+    for a, b in zip(ida, ast):
+        assert a["status"] == b["status"] == "solved" and a["cost"] == b["cost"]
+
+
+def test_rc_pdb_only_aidastar_solves_walks():
+    rc, rows, err = run(["--domain", "rc", "--walks", "3:5:7:9", "--model", "mlp:/dev/null", "--mode", "pdb",
+                         "--table1-pdb", "4", "--threads", "2", "--immediate"])
+    assert rc == 0, err
+    assert [r["status"] for r in rows] == ["solved"] * 3
+    assert all(r["cost"] <= 7 for r in rows)
+
+
+def test_gpu_mode_without_device_fails_cleanly(man3):
+    import paper_2507_11916_b200 as bida
+
+    if bida._native.lib().bida_gpu_device_count() > 0:
+        pytest.skip("a GPU is present")
+    rc, rows, err = run(["--domain", "stp3", "--walks", "1:5:5:1", "--model", "linear:" + man3, "--mode", "gpu"])
+    assert rc != 0 and "GpuBackend" in err
