@@ -35,10 +35,12 @@ WORKLOADS = {
     "rc-linear-e1-c21": dict(domain="rc", kind="linear", E=1, C=21, q=0.5, batch=1 << 22),
     "rc-linear-e4-c21": dict(domain="rc", kind="linear", E=4, C=21, q=0.5, batch=1 << 22),
     "stp4-linear-c72": dict(domain="stp4", kind="linear", E=1, C=72, q=0.5, batch=1 << 22),
-    # BMLP1 int8 MLPs; widths bracket the paper's 0.2 / 2.3 MB model-size anchors
+    # BMLP1 int8 MLPs; widths bracket the paper's 0.2 / 2.3 / 13.6 MB fp32 model-size
+    # anchors (H ~ 85 / 547 / 1610 at two hidden layers)
     "rc-mlp-h128": dict(domain="rc", kind="mlp", H=[128, 128], E=1, C=21, q=0.5, batch=1 << 22),
     "rc-mlp-h256": dict(domain="rc", kind="mlp", H=[256, 256], E=1, C=21, q=0.5, batch=1 << 22),
     "rc-mlp-h512": dict(domain="rc", kind="mlp", H=[512, 512], E=1, C=21, q=0.5, batch=1 << 22),
+    "rc-mlp-h1610": dict(domain="rc", kind="mlp", H=[1610, 1610], E=1, C=21, q=0.5, batch=1 << 21),
 }
 DEFAULT_WORKLOAD = "rc-mlp-h128"
 

@@ -131,7 +131,7 @@ int bida_gpu_attach_pdb_file(bida_gpu_evaluator *ev, const char *path, int mode)
 
 int bida_gpu_info(const bida_gpu_evaluator *ev, bida_gpu_model_info *out);
 /* Diagnostics (MLP handles): record a clock64 timeline of CTA 0's warps into
- * the DEVICE buffer `dev_buf` (int64 [warps][bida_gpu_trace_slots()]) on every
+ * the DEVICE buffer `dev_buf` (int64 [32 warps][bida_gpu_trace_slots()]) on every
  * subsequent launch; NULL switches it off. */
 int bida_gpu_debug_trace(bida_gpu_evaluator *ev, long long *dev_buf);
 int bida_gpu_trace_slots(void);

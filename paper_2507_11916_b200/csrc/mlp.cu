@@ -40,12 +40,13 @@ namespace bida_gpu {
 
 constexpr int kMaxMembers = 8;
 constexpr int kMaxLayers = 5;   // hidden layers <= 4
+constexpr int kMaxHidden = 4096;
 constexpr int kTileM = 128;
 constexpr int kMaxStages = 6;
 constexpr int kStageBytes = 16384;
 constexpr int kMlpThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2-9 two epilogue groups
 constexpr int kKChunk = 32;       // bytes of K per MMA instruction
-enum MlpMode { kPair = 0, kSplit = 1, kResident = 2 };
+enum MlpMode { kPair = 0, kSplit = 1, kResident = 2, kDuo = 3, kWide = 4 };
 
 struct MlpLayer {
     int K, N;          // padded input width (multiple of 32), output width (multiple of 16)
@@ -78,6 +79,8 @@ struct MlpParams {
     int *err;
     long long *trace;   // optional debug timeline (CTA 0): [warp][kTraceSlots] (clock64, tag)
     PdbArgs pdb;        // optional PDB correction (pdb.cuh)
+    uint8_t *scratch;   // wide: per-CTA hidden activations, 2 buffers of sbytes (global, L2-resident)
+    long long sbytes;
 };
 
 constexpr int kTraceSlots = 256;
@@ -601,6 +604,667 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
         sm100::tmem_dealloc(tmem, p.tmem_cols);
 }
 
+// ------------------------------------------------------------------ duo schedule
+// Hidden-layer epilogue of one thread (= TMEM lane = tile row) over columns
+// [c_beg, c_end): (acc + bias) >> shift, saturated to u8, stored as the next
+// layer's K-major A operand at `out`.  The TMEM load of the next 16 columns is
+// in flight while the current 16 are requantised and stored.
+__device__ __forceinline__ void requant_columns(uint32_t t_row, const int32_t *bias, int sh, uint32_t out, int row,
+                                                int c_beg, int c_end) {
+    auto requant = [&](const int32_t(&r)[16], const int4(&b4)[4], int c0) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            w[q] = sm100::pack_sat_u8x4((r[q * 4 + 0] + b4[q].x) >> sh, (r[q * 4 + 1] + b4[q].y) >> sh,
+                                        (r[q * 4 + 2] + b4[q].z) >> sh, (r[q * 4 + 3] + b4[q].w) >> sh);
+        sm100::st_shared_v4(out + (c0 >> 4) * 2048u + row * 16u, w[0], w[1], w[2], w[3]);
+    };
+    auto load_bias = [&](int4(&b4)[4], int c0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
+    };
+    int32_t ra[16], rb[16];
+    int4 ba[4], bb[4];
+    sm100::tmem_ld16(t_row + c_beg, ra);
+    load_bias(ba, c_beg);
+    sm100::tmem_wait_ld();
+    for (int c0 = c_beg; c0 < c_end; c0 += 32) {
+        const bool has_b = c0 + 16 < c_end;
+        if (has_b) {
+            sm100::tmem_ld16(t_row + c0 + 16, rb);
+            load_bias(bb, c0 + 16);
+        }
+        requant(ra, ba, c0);
+        sm100::tmem_wait_ld();
+        if (!has_b)
+            break;
+        if (c0 + 32 < c_end) {
+            sm100::tmem_ld16(t_row + c0 + 32, ra);
+            load_bias(ba, c0 + 32);
+        }
+        requant(rb, bb, c0 + 16);
+        sm100::tmem_wait_ld();
+    }
+}
+
+// kDuo: resident weights with TWO jobs in flight.  The CTA's tiles alternate
+// between two slots; slot s owns activation buffer s (the one-hot, then every
+// hidden activation aliased over it: a layer's input is dead once its MMAs
+// completed), TMEM columns [s*cols/2, +cols/2) and an epilogue group of 8
+// warps (two per TMEM lane quadrant: half 0 drains columns [0, N/2) and reads
+// out, half 1 drains [N/2, N) and encodes the slot's next job).  The MMA warp
+// serves whichever slot's input is ready, so one slot's epilogue overlaps the
+// other slot's MMAs.  Barriers per slot: act_ready (256 epilogue threads: the
+// layer input is written / the accumulator was read) and d_full (commit).
+constexpr int kDuoThreads = 544;  // warp 0: weight load + MMA issue; warps 1-16: two epilogue groups
+
+template <int DOMAIN, int CM>
+__global__ void __launch_bounds__(kDuoThreads, 1) mlp_duo_kernel(const __grid_constant__ MlpParams p) {
+    using T = DomainTraits<DOMAIN>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *wbuf = smem + 2 * p.xbytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(wbuf + p.wbytes_pad);
+    uint64_t *w_ready = bars;        // weight image landed
+    uint64_t *act_ready = bars + 1;  // [2]
+    uint64_t *d_full = bars + 3;     // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 5);
+
+    const int warp = threadIdx.x >> 5;
+    const long long ntiles = (p.n + kTileM - 1) / kTileM;
+    const long long nloc =
+        blockIdx.x < ntiles ? (ntiles - static_cast<long long>(blockIdx.x) + gridDim.x - 1) / gridDim.x : 0;
+    const uint32_t slot_cols = p.tmem_cols >> 1;
+
+    if (threadIdx.x == 0) {
+        sm100::mbar_init(w_ready, 1);
+        for (int s = 0; s < 2; ++s) {
+            sm100::mbar_init(&act_ready[s], 256);
+            sm100::mbar_init(&d_full[s], 1);
+        }
+        sm100::fence_barrier_init();
+    }
+    if (warp == 0)
+        sm100::tmem_alloc(tmem_slot, p.tmem_cols);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    Tracer tr;
+    if (p.trace && blockIdx.x == 0 && lane_id() == 0)
+        tr.buf = p.trace + static_cast<long long>(warp) * kTraceSlots;
+
+    if (warp == 0) {
+        // ------------------------------------------------ weight load + MMA issue
+        if (nloc > 0) {
+            if (lane_id() == 0) {
+                sm100::mbar_arrive_expect_tx(w_ready, static_cast<uint32_t>(p.wbytes));
+                for (int off = 0; off < p.wbytes; off += kStageBytes) {
+                    const int b = min(kStageBytes, p.wbytes - off);
+                    sm100::bulk_g2s(wbuf + off, p.wimg + off, static_cast<uint32_t>(b), w_ready);
+                }
+            }
+            __syncwarp();
+            sm100::mbar_wait(w_ready, 0);
+            const uint32_t sbase = sm100::smem_u32(smem), sW = sm100::smem_u32(wbuf);
+            long long k[2] = {0, 1};
+            int e[2] = {0, 0}, l[2] = {0, 0};
+            uint32_t aph[2] = {0u, 0u};
+            bool rem[2] = {nloc > 0, nloc > 1};
+            while (rem[0] || rem[1]) {
+                bool idle = true;
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    if (!rem[s] || !__any_sync(kFull, sm100::mbar_test_wait(&act_ready[s], aph[s])))
+                        continue;
+                    idle = false;
+                    sm100::mbar_wait(&act_ready[s], aph[s]);  // acquire on every lane
+                    aph[s] ^= 1u;
+                    if (lane_id() == 0)
+                        tr(20 + l[s] + 4 * s);
+                    sm100::tc_fence_after();
+                    const MlpLayer ly = p.layer[e[s]][l[s]];
+                    const int nch = ly.K / kKChunk;
+                    const uint32_t cbytes = static_cast<uint32_t>(ly.N) * kKChunk;
+                    const uint32_t idesc = sm100::make_idesc_i8(ly.N);
+                    uint64_t adesc = sm100::make_smem_desc(sbase + s * p.xbytes, 2048u, 128u);
+                    uint64_t bdesc = sm100::make_smem_desc(sW + static_cast<uint32_t>(ly.woff), cbytes >> 1, 128u);
+                    const uint32_t dcol = tmem + s * slot_cols;
+                    if (sm100::elect_one()) {
+                        for (int j = 0; j < nch; ++j) {
+                            sm100::mma_i8(dcol, adesc, bdesc, idesc, j > 0 ? 1u : 0u);
+                            adesc += 4096u >> 4;
+                            bdesc += cbytes >> 4;
+                        }
+                        sm100::mma_commit(&d_full[s]);
+                    }
+                    __syncwarp();
+                    if (lane_id() == 0)
+                        tr(30 + l[s] + 4 * s);
+                    if (++l[s] == p.nl) {
+                        l[s] = 0;
+                        if (++e[s] == p.E) {
+                            e[s] = 0;
+                            k[s] += 2;
+                            rem[s] = k[s] < nloc;
+                        }
+                    }
+                }
+                if (idle)
+                    __nanosleep(32);  // leave the issue slots to this SM sub-partition's epilogue warps
+            }
+        }
+    } else {
+        // ------------------------------------------------ encode / epilogue / readout
+        const int ew = warp - 1;
+        const int g = ew >> 3;          // slot
+        const int half = (ew >> 2) & 1; // 0: drains [0, N/2) + reads out; 1: drains [N/2, N) + encodes
+        const int quad = warp & 3;      // TMEM lane quadrant this warp may access
+        const int row = quad * 32 + lane_id();
+        const uint32_t sX = sm100::smem_u32(smem) + g * p.xbytes;
+        const uint32_t t_row = tmem + g * slot_cols + (static_cast<uint32_t>(quad * 32) << 16);
+        uint64_t *my_ready = &act_ready[g];
+        uint64_t *my_full = &d_full[g];
+        uint32_t dph = 0;
+
+        auto load_state = [&](long long kk, uint64_t &lo_, uint64_t &hi_) {
+            lo_ = hi_ = 0;
+            const long long s_ = (blockIdx.x + kk * gridDim.x) * kTileM + row;
+            if (kk < nloc && s_ < p.n) {
+                if constexpr (T::PB == 16) {
+                    const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2 *>(p.packed) + s_);
+                    lo_ = v.x;
+                    hi_ = v.y;
+                } else {
+                    lo_ = __ldcs(reinterpret_cast<const unsigned long long *>(p.packed) + s_);
+                }
+            }
+        };
+        auto state_bad = [&](uint64_t lo_, uint64_t hi_) {
+            bool b = false;
+#pragma unroll
+            for (int q = 0; q < T::NNZ; ++q) {
+                const int j = position_feature<DOMAIN>(lo_, hi_, q);
+                b |= j < 0 || j >= T::F;
+            }
+            return b;
+        };
+        auto tile_valid = [&](long long kk) { return kk < nloc && (blockIdx.x + kk * gridDim.x) * kTileM + row < p.n; };
+        const int nchunk = p.Fpad / 16;
+        auto encode = [&](uint64_t lo_, uint64_t hi_, bool live_) {
+            tr(40);
+            for (int c16 = 0; c16 < nchunk; ++c16)
+                sm100::st_shared_v4(sX + c16 * 2048u + row * 16u, 0u, 0u, 0u, 0u);
+            if (live_) {
+#pragma unroll
+                for (int q = 0; q < T::NNZ; ++q) {
+                    const int j = position_feature<DOMAIN>(lo_, hi_, q);
+                    sm100::st_shared_u8(sX + (j >> 4) * 2048u + row * 16u + (j & 15), 1u);
+                }
+            }
+            sm100::fence_proxy_async_smem();
+            tr(41);
+            sm100::mbar_arrive(my_ready);
+        };
+
+        uint64_t nlo = 0, nhi = 0;
+        load_state(g, nlo, nhi);
+        if (g < nloc) {  // the slot's first job: half 1 encodes, half 0 has nothing to drain
+            if (half)
+                encode(nlo, nhi, tile_valid(g) && !state_bad(nlo, nhi));
+            else
+                sm100::mbar_arrive(my_ready);
+        }
+        for (long long k = g; k < nloc; k += 2) {
+            const long long st = (blockIdx.x + k * gridDim.x) * kTileM + row;
+            const bool valid = st < p.n;
+            const uint64_t lo = nlo, hi = nhi;
+            load_state(k + 2, nlo, nhi);
+            const bool bad = valid && state_bad(lo, hi);
+            const bool reader = half == 0;
+            const int hpdb = (p.pdb.entries && reader && valid) ? pdb_fetch<DOMAIN>(p.pdb, lo) : 0;
+            if (bad && reader)
+                raise_error(p.err, kErrState);
+            const bool live = valid && !bad;
+            int hmin = 0x7fffffff;
+            bool dist_bad = false;
+            for (int e = 0; e < p.E; ++e) {
+                for (int l = 0; l < p.nl; ++l) {
+                    const MlpLayer &ly = p.layer[e][l];
+                    tr(50 + l);
+                    sm100::mbar_wait(my_full, dph);
+                    dph ^= 1u;
+                    tr(60 + l);
+                    sm100::tc_fence_after();
+                    const int32_t *bias = p.bias + ly.boff;
+                    if (l + 1 < p.nl) {
+                        const int hN = ly.N >> 1;
+                        requant_columns(t_row, bias, ly.shift, sX, row, half * hN, half * hN + hN);
+                        sm100::tc_fence_before();
+                        sm100::fence_proxy_async_smem();
+                        tr(70 + l);
+                        sm100::mbar_arrive(my_ready);
+                        continue;
+                    }
+                    const bool next_member = e + 1 < p.E;
+                    const bool has_next = next_member || k + 2 < nloc;
+                    if (!reader) {
+                        // the slot's next job: X is free (this job's last MMAs completed)
+                        if (has_next) {
+                            if (next_member)
+                                encode(lo, hi, live);
+                            else
+                                encode(nlo, nhi, tile_valid(k + 2) && !state_bad(nlo, nhi));
+                        }
+                        continue;
+                    }
+                    // output layer: exact integer logits -> certified readout
+                    int32_t v[CM];
+#pragma unroll
+                    for (int c0 = 0; c0 < CM; c0 += 16) {
+                        if (c0 < p.C) {
+                            int32_t r[16];
+                            sm100::tmem_ld16(t_row + c0, r);
+                            int4 b4[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
+                            sm100::tmem_wait_ld();
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                v[c0 + 4 * q + 0] = r[4 * q + 0] + b4[q].x;
+                                v[c0 + 4 * q + 1] = r[4 * q + 1] + b4[q].y;
+                                v[c0 + 4 * q + 2] = r[4 * q + 2] + b4[q].z;
+                                v[c0 + 4 * q + 3] = r[4 * q + 3] + b4[q].w;
+                            }
+                        }
+                    }
+                    sm100::tc_fence_before();
+                    if (has_next)
+                        sm100::mbar_arrive(my_ready);  // accumulator read: the next job's L0 may start
+                    tr(81);
+                    if (p.logits_out && valid) {
+                        double *dst = p.logits_out + (static_cast<size_t>(st) * p.E + e) * p.C;
+                        for (int c = 0; c < p.C; ++c)
+                            dst[c] = static_cast<double>(v[c]) * p.scale_d[e];
+                    }
+                    bool fb = false;
+                    const int h = readout_certified<CM>(v, p.C, p.scale_f[e], p.scale_d[e], p.rk, &dist_bad, &fb);
+                    hmin = min(hmin, h);
+                    tr(fb ? 83 : 82);
+                    tr(80);
+                }
+            }
+            if (reader && valid) {
+                if (dist_bad)
+                    raise_error(p.err, kErrDistribution);
+                int h = (live && !dist_bad) ? hmin : 0;
+                if (p.pdb.entries && live) {
+                    if (hpdb < 0) {
+                        raise_error(p.err, kErrState);
+                        h = 0;
+                    } else {
+                        h = pdb_combine(p.pdb, h, hpdb);
+                    }
+                }
+                p.h_out[st] = h;
+            }
+        }
+    }
+
+    __syncwarp();
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    if (warp == 0)
+        sm100::tmem_dealloc(tmem, p.tmem_cols);
+}
+
+// ------------------------------------------------------------------ wide schedule
+// kWide: hidden layers of any width up to kMaxHidden.  A tile's activations
+// no longer fit in shared memory (128 x 1664 B = 208 KB for the paper's
+// 13.6 MB model), so every layer l >= 1 streams its A operand from a per-CTA
+// global scratch buffer (L2-resident, written by the previous layer's
+// epilogue in the UMMA core-matrix layout) together with the weights: a stage
+// is one 32-byte K step = [A 128x32 B][B chunk x 32 B].  Output columns are
+// produced in chunks of 512 (two N <= 256 MMAs into TMEM columns [0,256) and
+// [256,512)); epilogue group g drains half g of each chunk.  Layer 0 reads the
+// one-hot tile X from shared memory, as in the other schedules.
+constexpr int kWideChunk = 512;
+constexpr int kWideStageA = 128 * kKChunk;                   // 4 KB
+constexpr int kWideStage = kWideStageA + kWideChunk * kKChunk;  // 20 KB
+constexpr int kWideMaxStages = 10;
+
+// Hidden-layer epilogue into global scratch: TMEM columns [t0, t0 + n) hold
+// output columns [o0, o0 + n) of this thread's row.
+__device__ __forceinline__ void requant_to_global(uint32_t t_row, int t0, const int32_t *bias, int o0, int n, int sh,
+                                                  uint8_t *out, int row) {
+    auto store = [&](const int32_t(&r)[16], const int4(&b4)[4], int oc) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            w[q] = sm100::pack_sat_u8x4((r[q * 4 + 0] + b4[q].x) >> sh, (r[q * 4 + 1] + b4[q].y) >> sh,
+                                        (r[q * 4 + 2] + b4[q].z) >> sh, (r[q * 4 + 3] + b4[q].w) >> sh);
+        sm100::st_global_v4(out + (oc >> 5) * 4096 + ((oc >> 4) & 1) * 2048 + row * 16, w[0], w[1], w[2], w[3]);
+    };
+    auto load_bias = [&](int4(&b4)[4], int oc) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + oc) + q);
+    };
+    int32_t ra[16], rb[16];
+    int4 ba[4], bb[4];
+    sm100::tmem_ld16(t_row + t0, ra);
+    load_bias(ba, o0);
+    sm100::tmem_wait_ld();
+    for (int j = 0; j < n; j += 32) {
+        const bool has_b = j + 16 < n;
+        if (has_b) {
+            sm100::tmem_ld16(t_row + t0 + j + 16, rb);
+            load_bias(bb, o0 + j + 16);
+        }
+        store(ra, ba, o0 + j);
+        sm100::tmem_wait_ld();
+        if (!has_b)
+            break;
+        if (j + 32 < n) {
+            sm100::tmem_ld16(t_row + t0 + j + 32, ra);
+            load_bias(ba, o0 + j + 32);
+        }
+        store(rb, bb, o0 + j + 16);
+        sm100::tmem_wait_ld();
+    }
+}
+
+template <int DOMAIN, int CM>
+__global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_constant__ MlpParams p) {
+    using T = DomainTraits<DOMAIN>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *stages = smem + p.xbytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stages + p.stages * kWideStage);
+    uint64_t *full = bars;                        // [kWideMaxStages]
+    uint64_t *empty = bars + kWideMaxStages;      // [kWideMaxStages]
+    uint64_t *x_ready = bars + 2 * kWideMaxStages;  // one-hot of the tile written (group 1)
+    uint64_t *d_full = x_ready + 1;               // chunk accumulator complete (commit)
+    uint64_t *tmem_free = d_full + 1;             // chunk drained (256 epilogue threads)
+    uint64_t *act_done = tmem_free + 1;           // hidden layer written to scratch (256)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(act_done + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const long long ntiles = (p.n + kTileM - 1) / kTileM;
+    const long long nloc =
+        blockIdx.x < ntiles ? (ntiles - static_cast<long long>(blockIdx.x) + gridDim.x - 1) / gridDim.x : 0;
+    uint8_t *scr = p.scratch + static_cast<long long>(blockIdx.x) * 2 * p.sbytes;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kWideMaxStages; ++s) {
+            sm100::mbar_init(&full[s], 1);
+            sm100::mbar_init(&empty[s], 1);
+        }
+        sm100::mbar_init(x_ready, 128);
+        sm100::mbar_init(d_full, 1);
+        sm100::mbar_init(tmem_free, 256);
+        sm100::mbar_init(act_done, 256);
+        sm100::fence_barrier_init();
+    }
+    if (warp == 1)
+        sm100::tmem_alloc(tmem_slot, 512);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    Tracer tr;
+    if (p.trace && blockIdx.x == 0 && lane_id() == 0)
+        tr.buf = p.trace + static_cast<long long>(warp) * kTraceSlots;
+
+    if (warp == 0) {
+        // ------------------------------------------------ producer: [A k-step][B chunk k-step] stages
+        if (lane_id() == 0 && nloc > 0) {
+            int s = 0;
+            uint32_t ph = 0, adph = 0;
+            for (long long k = 0; k < nloc; ++k)
+                for (int e = 0; e < p.E; ++e)
+                    for (int l = 0; l < p.nl; ++l) {
+                        const MlpLayer &ly = p.layer[e][l];
+                        const int nk = ly.K / kKChunk;
+                        const uint8_t *a_src = scr + ((l - 1) & 1) * p.sbytes;
+                        if (l > 0) {  // the previous layer's activations are in scratch
+                            sm100::mbar_wait(act_done, adph);
+                            adph ^= 1u;
+                        }
+                        for (int c0 = 0; c0 < ly.N; c0 += kWideChunk) {
+                            const int cw = min(kWideChunk, ly.N - c0);
+                            const uint8_t *b_src = p.wimg + ly.woff + static_cast<long long>(c0) * ly.K;
+                            for (int kc = 0; kc < nk; ++kc) {
+                                sm100::mbar_wait(&empty[s], ph ^ 1u);
+                                uint8_t *st = stages + s * kWideStage;
+                                sm100::mbar_arrive_expect_tx(&full[s], (l > 0 ? kWideStageA : 0) + cw * kKChunk);
+                                if (l > 0)
+                                    sm100::bulk_g2s(st, a_src + kc * kWideStageA, kWideStageA, &full[s]);
+                                sm100::bulk_g2s(st + kWideStageA, b_src + kc * cw * kKChunk, cw * kKChunk, &full[s]);
+                                if (++s == p.stages) {
+                                    s = 0;
+                                    ph ^= 1u;
+                                }
+                            }
+                        }
+                    }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (nloc > 0) {
+            int s = 0;
+            uint32_t ph = 0, xph = 0, tfph = 0;
+            const uint32_t sX = sm100::smem_u32(smem), sS = sm100::smem_u32(stages);
+            for (long long k = 0; k < nloc; ++k)
+                for (int e = 0; e < p.E; ++e)
+                    for (int l = 0; l < p.nl; ++l) {
+                        const MlpLayer ly = p.layer[e][l];
+                        const int nk = ly.K / kKChunk;
+                        if (l == 0 && e == 0) {
+                            if (lane_id() == 0)
+                                tr(10);
+                            sm100::mbar_wait(x_ready, xph);
+                            xph ^= 1u;
+                        }
+                        for (int c0 = 0; c0 < ly.N; c0 += kWideChunk) {
+                            const int cw = min(kWideChunk, ly.N - c0);
+                            const int w0 = min(256, cw), w1 = cw - w0;
+                            const uint32_t id0 = sm100::make_idesc_i8(w0), id1 = sm100::make_idesc_i8(w1 > 0 ? w1 : 16);
+                            sm100::mbar_wait(tmem_free, tfph ^ 1u);  // previous chunk drained
+                            tfph ^= 1u;
+                            if (lane_id() == 0)
+                                tr(20 + l);
+                            sm100::tc_fence_after();
+                            uint64_t xdesc = sm100::make_smem_desc(sX, 2048u, 128u);
+                            for (int kc = 0; kc < nk; ++kc) {
+                                sm100::mbar_wait(&full[s], ph);
+                                sm100::tc_fence_after();
+                                const uint32_t st = sS + s * kWideStage;
+                                const uint64_t adesc = l == 0 ? xdesc : sm100::make_smem_desc(st, 2048u, 128u);
+                                const uint64_t b0 = sm100::make_smem_desc(st + kWideStageA, w0 * 16u, 128u);
+                                const uint64_t b1 = sm100::make_smem_desc(st + kWideStageA + w0 * kKChunk, w1 * 16u, 128u);
+                                if (sm100::elect_one()) {
+                                    sm100::mma_i8(tmem, adesc, b0, id0, kc > 0 ? 1u : 0u);
+                                    if (w1 > 0)
+                                        sm100::mma_i8(tmem + 256, adesc, b1, id1, kc > 0 ? 1u : 0u);
+                                    sm100::mma_commit(&empty[s]);
+                                }
+                                __syncwarp();
+                                xdesc += 4096u >> 4;
+                                if (++s == p.stages) {
+                                    s = 0;
+                                    ph ^= 1u;
+                                }
+                            }
+                            if (sm100::elect_one())
+                                sm100::mma_commit(d_full);
+                            __syncwarp();
+                            if (lane_id() == 0)
+                                tr(30 + l);
+                        }
+                    }
+        }
+    } else {
+        // ------------------------------------------------ encode / epilogue / readout
+        const int grp = (warp - 2) >> 2;  // drains TMEM half grp of every chunk
+        const int quad = warp & 3;
+        const int row = quad * 32 + lane_id();
+        const uint32_t sX = sm100::smem_u32(smem);
+        const uint32_t t_row = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+        uint32_t dph = 0;
+        const bool reader = grp == 0, encoder = grp == 1;
+
+        auto load_state = [&](long long kk, uint64_t &lo_, uint64_t &hi_) {
+            lo_ = hi_ = 0;
+            const long long s_ = (blockIdx.x + kk * gridDim.x) * kTileM + row;
+            if (kk < nloc && s_ < p.n) {
+                if constexpr (T::PB == 16) {
+                    const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2 *>(p.packed) + s_);
+                    lo_ = v.x;
+                    hi_ = v.y;
+                } else {
+                    lo_ = __ldcs(reinterpret_cast<const unsigned long long *>(p.packed) + s_);
+                }
+            }
+        };
+        auto state_bad = [&](uint64_t lo_, uint64_t hi_) {
+            bool b = false;
+#pragma unroll
+            for (int q = 0; q < T::NNZ; ++q) {
+                const int j = position_feature<DOMAIN>(lo_, hi_, q);
+                b |= j < 0 || j >= T::F;
+            }
+            return b;
+        };
+        auto tile_valid = [&](long long kk) { return kk < nloc && (blockIdx.x + kk * gridDim.x) * kTileM + row < p.n; };
+        const int nchunk16 = p.Fpad / 16;
+        auto encode = [&](uint64_t lo_, uint64_t hi_, bool live_) {
+            tr(40);
+            for (int c16 = 0; c16 < nchunk16; ++c16)
+                sm100::st_shared_v4(sX + c16 * 2048u + row * 16u, 0u, 0u, 0u, 0u);
+            if (live_) {
+#pragma unroll
+                for (int q = 0; q < T::NNZ; ++q) {
+                    const int j = position_feature<DOMAIN>(lo_, hi_, q);
+                    sm100::st_shared_u8(sX + (j >> 4) * 2048u + row * 16u + (j & 15), 1u);
+                }
+            }
+            sm100::fence_proxy_async_smem();
+            tr(41);
+            sm100::mbar_arrive(x_ready);
+        };
+
+        uint64_t nlo = 0, nhi = 0;
+        load_state(0, nlo, nhi);
+        if (encoder && nloc > 0)
+            encode(nlo, nhi, tile_valid(0) && !state_bad(nlo, nhi));
+        for (long long k = 0; k < nloc; ++k) {
+            const long long st = (blockIdx.x + k * gridDim.x) * kTileM + row;
+            const bool valid = st < p.n;
+            const uint64_t lo = nlo, hi = nhi;
+            load_state(k + 1, nlo, nhi);
+            const bool bad = valid && state_bad(lo, hi);
+            const int hpdb = (p.pdb.entries && reader && valid) ? pdb_fetch<DOMAIN>(p.pdb, lo) : 0;
+            if (bad && reader)
+                raise_error(p.err, kErrState);
+            const bool live = valid && !bad;
+            int hmin = 0x7fffffff;
+            bool dist_bad = false;
+            for (int e = 0; e < p.E; ++e) {
+                for (int l = 0; l < p.nl; ++l) {
+                    const MlpLayer &ly = p.layer[e][l];
+                    const int32_t *bias = p.bias + ly.boff;
+                    const bool hidden = l + 1 < p.nl;
+                    uint8_t *out = scr + (l & 1) * p.sbytes;
+                    for (int c0 = 0; c0 < ly.N; c0 += kWideChunk) {
+                        const int cw = min(kWideChunk, ly.N - c0);
+                        const int w0 = min(256, cw);
+                        tr(50 + l);
+                        sm100::mbar_wait(d_full, dph);
+                        dph ^= 1u;
+                        tr(60 + l);
+                        sm100::tc_fence_after();
+                        if (hidden) {
+                            const int t0 = grp ? 256 : 0, n = grp ? cw - w0 : w0;
+                            if (n > 0)
+                                requant_to_global(t_row, t0, bias, c0 + t0, n, ly.shift, out, row);
+                            sm100::tc_fence_before();
+                            sm100::mbar_arrive(tmem_free);
+                            tr(70 + l);
+                            continue;
+                        }
+                        // output layer (one chunk, C <= 256 columns in half 0)
+                        if (!reader) {
+                            sm100::tc_fence_before();
+                            sm100::mbar_arrive(tmem_free);
+                            continue;
+                        }
+                        int32_t v[CM];
+#pragma unroll
+                        for (int q0 = 0; q0 < CM; q0 += 16) {
+                            if (q0 < p.C) {
+                                int32_t r[16];
+                                sm100::tmem_ld16(t_row + q0, r);
+                                int4 b4[4];
+#pragma unroll
+                                for (int q = 0; q < 4; ++q)
+                                    b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + q0) + q);
+                                sm100::tmem_wait_ld();
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    v[q0 + 4 * q + 0] = r[4 * q + 0] + b4[q].x;
+                                    v[q0 + 4 * q + 1] = r[4 * q + 1] + b4[q].y;
+                                    v[q0 + 4 * q + 2] = r[4 * q + 2] + b4[q].z;
+                                    v[q0 + 4 * q + 3] = r[4 * q + 3] + b4[q].w;
+                                }
+                            }
+                        }
+                        sm100::tc_fence_before();
+                        sm100::mbar_arrive(tmem_free);
+                        if (p.logits_out && valid) {
+                            double *dst = p.logits_out + (static_cast<size_t>(st) * p.E + e) * p.C;
+                            for (int c = 0; c < p.C; ++c)
+                                dst[c] = static_cast<double>(v[c]) * p.scale_d[e];
+                        }
+                        bool fb = false;
+                        const int h = readout_certified<CM>(v, p.C, p.scale_f[e], p.scale_d[e], p.rk, &dist_bad, &fb);
+                        hmin = min(hmin, h);
+                        tr(80);
+                    }
+                    if (hidden) {
+                        sm100::fence_proxy_async_global();  // scratch writes -> the producer's bulk reads
+                        sm100::mbar_arrive(act_done);
+                    }
+                    if (l == 0 && e + 1 == p.E && encoder && k + 1 < nloc)
+                        encode(nlo, nhi, tile_valid(k + 1) && !state_bad(nlo, nhi));  // X free: layer 0 done
+                }
+            }
+            if (reader && valid) {
+                if (dist_bad)
+                    raise_error(p.err, kErrDistribution);
+                int h = (live && !dist_bad) ? hmin : 0;
+                if (p.pdb.entries && live) {
+                    if (hpdb < 0) {
+                        raise_error(p.err, kErrState);
+                        h = 0;
+                    } else {
+                        h = pdb_combine(p.pdb, h, hpdb);
+                    }
+                }
+                p.h_out[st] = h;
+            }
+        }
+    }
+
+    __syncwarp();
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    if (warp == 1)
+        sm100::tmem_dealloc(tmem, 512);
+}
+
 // ------------------------------------------------------------------ host
 
 namespace {
@@ -616,7 +1280,14 @@ uint32_t rd32(const unsigned char *b) {
 
 template <int DOMAIN, int CM>
 int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
-    auto kern = mlp_fused_kernel<DOMAIN, CM>;
+    auto kern = p.mode == kWide ? mlp_wide_kernel<DOMAIN, CM> : mlp_fused_kernel<DOMAIN, CM>;
+    int threads = kMlpThreads;
+    if constexpr (CM == 32) {  // the duo schedule is built for C <= 32 (register budget at 544 threads)
+        if (p.mode == kDuo) {
+            kern = mlp_duo_kernel<DOMAIN, CM>;
+            threads = kDuoThreads;
+        }
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(m->smem));
     if (e != cudaSuccess) {
@@ -625,6 +1296,14 @@ int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
     }
     const long long ntiles = (p.n + kTileM - 1) / kTileM;
     int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(ntiles, m->grid_cap)));
+    MlpParams q = p;
+    if (p.mode == kWide) {  // per-launch scratch from the stream-ordered pool (concurrent launches are safe)
+        e = cudaMallocAsync(reinterpret_cast<void **>(&q.scratch), static_cast<size_t>(grid) * 2 * p.sbytes, st);
+        if (e != cudaSuccess) {
+            g_err = std::string("mlp scratch: ") + cudaGetErrorString(e);
+            return 1;
+        }
+    }
     if (p.cluster == 2) {
         grid = (grid + 1) & ~1;
         cudaLaunchConfig_t cfg = {};
@@ -639,12 +1318,17 @@ int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kern, p);
+        e = cudaLaunchKernelEx(&cfg, kern, q);
     } else {
-        kern<<<grid, kMlpThreads, m->smem, st>>>(p);
+        kern<<<grid, threads, m->smem, st>>>(q);
     }
     if (e == cudaSuccess)
         e = cudaGetLastError();
+    if (p.mode == kWide) {
+        const cudaError_t fe = cudaFreeAsync(q.scratch, st);
+        if (e == cudaSuccess)
+            e = fe;
+    }
     if (e != cudaSuccess) {
         g_err = std::string("mlp launch: ") + cudaGetErrorString(e);
         return 1;
@@ -684,10 +1368,13 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     for (uint32_t l = 0; l < L; ++l) {
         H[l] = static_cast<int>(rd32(b + off));
         off += 4;
-        if (H[l] < 32 || H[l] > 512 || H[l] % 32)
-            return fail(err, 1, "BMLP1: hidden widths must be multiples of 32 in [32, 512]");
+        if (H[l] < 1 || H[l] > kMaxHidden)
+            return fail(err, 1, "BMLP1: hidden widths must be in [1, 4096]");
     }
     const int Fpad = (F + 31) / 32 * 32;
+    std::vector<int> Hp(L);  // widths padded to the 32-byte MMA K step (zero weights and bias)
+    for (uint32_t l = 0; l < L; ++l)
+        Hp[l] = (H[l] + 31) / 32 * 32;
     const int Cpad = std::max(16, (static_cast<int>(C) + 15) / 16 * 16);
     const int nl = static_cast<int>(L) + 1;
     auto *m = new MlpModel();
@@ -699,11 +1386,11 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     p.Fpad = Fpad;
     int KX = Fpad, KY = 0, Nmax = Cpad;  // KX: even-layer inputs, KY: odd-layer inputs
     for (uint32_t l = 0; l < L; ++l) {
-        Nmax = std::max(Nmax, H[l]);
+        Nmax = std::max(Nmax, Hp[l]);
         if ((l + 1) % 2 == 0)
-            KX = std::max(KX, H[l]);
+            KX = std::max(KX, Hp[l]);
         else
-            KY = std::max(KY, H[l]);
+            KY = std::max(KY, Hp[l]);
     }
     std::vector<uint8_t> img;
     std::vector<int32_t> bias;
@@ -717,8 +1404,8 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
         for (int l = 0; l < nl; ++l) {
             const int in = l ? H[l - 1] : F;
             const int outn = l < static_cast<int>(L) ? H[l] : static_cast<int>(C);
-            const int K = l ? H[l - 1] : Fpad;
-            const int N = l < static_cast<int>(L) ? H[l] : Cpad;
+            const int K = l ? Hp[l - 1] : Fpad;
+            const int N = l < static_cast<int>(L) ? Hp[l] : Cpad;
             const size_t nw = static_cast<size_t>(in) * outn;
             if (len < off + nw + 4ull * outn) {
                 delete m;
@@ -791,17 +1478,48 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
             c <<= 1;
         return c;
     };
+    // 0) a layer wider than 512 (or nothing else fits): wide (activations in
+    //    L2-resident global scratch, A and B streamed)
     // 1) every layer <= 256 wide and the whole weight image fits next to one
     //    activation set: resident
     // 2) every layer <= 256 wide and two activation sets fit: pair (streamed)
-    // 3) otherwise: split (streamed)
-    // BIDA_MLP_FORCE_MODE=resident|pair|split (tests): use that schedule when it fits
+    // 3) every layer <= 512 wide: split (streamed)
+    // BIDA_MLP_FORCE_MODE=wide|duo|resident|pair|split (tests): use that schedule
+    // when it fits.  duo (two resident-weight jobs in flight, C <= 32) is
+    // opt-in only: measured slower than resident (profiles/r1_notes.md).
     const char *force = std::getenv("BIDA_MLP_FORCE_MODE");
     const std::string fm = force ? force : "";
+    int Kmax = Fpad;
+    for (uint32_t l = 0; l < L; ++l)
+        Kmax = std::max(Kmax, Hp[l]);
+    const size_t xduo = static_cast<size_t>(kTileM) * Kmax;  // one aliased activation buffer per slot
+    const bool fit_duo = Nmax <= 256 && C <= 32 && 2 * xduo + p.wbytes_pad + bar_bytes <= budget;
     const bool fit_res = Nmax <= 256 && set1 + p.wbytes_pad + bar_bytes <= budget;
     const bool fit_pair = Nmax <= 256 && stages_for(2 * set1) >= 2;
     const bool want_split = fm == "split" && stages_for(set1) >= 2;
-    if (!want_split && fit_res && (fm.empty() || fm == "resident" || (fm == "pair" && !fit_pair))) {  // (TMEM double-buffered by job)
+    const bool fit_split = Nmax <= 512 && stages_for(set1) >= 2;
+    const size_t wide_bars = 8 * (2 * kWideMaxStages + 4) + 16;
+    const size_t xwide = static_cast<size_t>(kTileM) * Fpad;
+    const int wide_stages =
+        xwide + wide_bars + 2 * kWideStage > budget
+            ? 0
+            : static_cast<int>(std::min<size_t>(kWideMaxStages, (budget - xwide - wide_bars) / kWideStage));
+    if (wide_stages >= 2 && (fm == "wide" || Nmax > 512 || (!fit_res && !fit_pair && !fit_split))) {
+        p.mode = kWide;
+        p.stages = wide_stages;
+        p.xbytes = static_cast<int>(xwide);
+        p.ybytes = 0;
+        p.tmem_cols = 512u;
+        p.sbytes = static_cast<long long>(kTileM) * Kmax;
+        m->smem = xwide + static_cast<size_t>(wide_stages) * kWideStage + wide_bars;
+    } else if (fit_duo && fm == "duo") {  // two jobs in flight, resident weights (opt-in: see r1_notes.md)
+        p.mode = kDuo;
+        p.stages = 0;
+        p.xbytes = static_cast<int>(xduo);
+        p.ybytes = 0;
+        p.tmem_cols = 2 * pow2cols(Nmax);
+        m->smem = 2 * xduo + p.wbytes_pad + bar_bytes;
+    } else if (!want_split && fit_res && (fm.empty() || fm == "resident" || fm == "duo" || (fm == "pair" && !fit_pair))) {  // (TMEM double-buffered by job)
         p.mode = kResident;
         p.stages = 0;
         p.tmem_cols = 512u;
@@ -811,7 +1529,7 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
         p.stages = stages_for(2 * set1);
         p.tmem_cols = 512;
         m->smem = 2 * set1 + static_cast<size_t>(p.stages) * kStageBytes + bar_bytes;
-    } else if (stages_for(set1) >= 2) {
+    } else if (fit_split) {
         p.mode = kSplit;
         p.stages = stages_for(set1);
         p.tmem_cols = pow2cols(Nmax);
@@ -830,6 +1548,35 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
             for (int l = 0; l < nl; ++l) {
                 MlpLayer &ly = p.layer[e][l];
                 const WSrc &w = wsrc[static_cast<size_t>(e) * nl + l];
+                if (p.mode == kWide) {
+                    // chunks of <= 512 output columns, each K/32 steps of
+                    // [half 0: w0 rows x 32 B][half 1: w1 rows x 32 B] (core-matrix layout)
+                    ly.nh = 1;
+                    ly.cps = 1;
+                    ly.woff = static_cast<long long>(pos0);
+                    for (int c0 = 0; c0 < ly.N; c0 += kWideChunk) {
+                        const int cw = std::min(kWideChunk, ly.N - c0), w0 = std::min(256, cw), w1 = cw - w0;
+                        for (int kc = 0; kc < ly.K / 32; ++kc) {
+                            const size_t base = pos0 + static_cast<size_t>(c0) * ly.K + static_cast<size_t>(kc) * cw * 32;
+                            for (int nn = 0; nn < cw; ++nn) {
+                                const int n = c0 + nn;
+                                if (n >= w.outn)
+                                    continue;
+                                const bool h1 = nn >= w0;
+                                const int hw = h1 ? w1 : w0, r = h1 ? nn - w0 : nn;
+                                for (int k = 0; k < 32; ++k) {
+                                    const int kk = kc * 32 + k;
+                                    if (kk >= w.in)
+                                        continue;
+                                    img[base + (h1 ? w0 * 32 : 0) + (k / 16) * (hw * 16) + (r / 8) * 128 + (r % 8) * 16 +
+                                        (k % 16)] = static_cast<uint8_t>(w.W[static_cast<size_t>(n) * w.in + kk]);
+                                }
+                            }
+                        }
+                    }
+                    pos0 += static_cast<size_t>(ly.N) * ly.K;
+                    continue;
+                }
                 ly.nh = (p.mode == kSplit && l + 1 < nl) ? 2 : 1;
                 const int Nh = ly.N / ly.nh;
                 ly.cps = std::max(1, kStageBytes / (Nh * kKChunk));
@@ -857,9 +1604,11 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     // 1.16 vs 1.26 G evals/s) -- the pair's lockstep costs more than the halved
     // per-SM copy issue saves (profiles/r1_notes.md).
     const char *mcv = std::getenv("BIDA_MLP_MULTICAST");
-    p.cluster = (p.mode != kResident && mcv && mcv[0] == '1') ? 2 : 1;
+    p.cluster = ((p.mode == kPair || p.mode == kSplit) && mcv && mcv[0] == '1') ? 2 : 1;
     m->cm = C <= 32 ? 32 : (C <= 64 ? 64 : 256);
     m->grid_cap = num_sms;
+    if (const char *mc = std::getenv("BIDA_MLP_MAX_CTAS"))  // tests: many tiles per CTA on small batches
+        m->grid_cap = std::max(1, std::min(num_sms, std::atoi(mc)));
     cudaError_t ce = cudaMalloc(&m->d_wimg, img.size());
     if (ce == cudaSuccess)
         ce = cudaMemcpy(m->d_wimg, img.data(), img.size(), cudaMemcpyHostToDevice);
@@ -870,6 +1619,16 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     if (ce != cudaSuccess) {
         mlp_destroy(m);
         return fail(err, 3, std::string("BMLP1 upload: ") + cudaGetErrorString(ce));
+    }
+    if (p.mode == kWide) {
+        // scratch comes from the device's stream-ordered pool per launch: keep
+        // freed blocks in the pool instead of returning them at every sync
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
     }
     p.wimg = m->d_wimg;
     p.bias = m->d_bias;

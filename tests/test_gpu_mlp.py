@@ -120,21 +120,21 @@ def test_device_resident(orc):
 
 def test_bad_models_rejected():
     with pytest.raises(ValueError):
-        bida.MlpModelBackend("rc", make_bmlp1("rc", hidden=[100], classes=21, seed=1), 0.5)  # not /32
+        bida.MlpModelBackend("rc", make_bmlp1("rc", hidden=[4097], classes=21, seed=1), 0.5)  # > 4096
     with pytest.raises(RuntimeError):
         bida.MlpModelBackend("rc", b"BMLP1" + b"\0" * 8, 0.5)
     with pytest.raises(RuntimeError):
         bida.MlpModelBackend("stp4", make_bmlp1("rc", hidden=[64], classes=21, seed=1), 0.5)
 
 
-@pytest.mark.parametrize("schedule", ["resident", "pair", "split"])
+@pytest.mark.parametrize("schedule", ["wide", "duo", "resident", "pair", "split"])
 @pytest.mark.parametrize(
     "hidden,C,E",
     [([128, 128], 21, 1), ([96, 160], 21, 1), ([64, 256, 96], 27, 2), ([256, 64], 40, 1), ([32], 7, 3)],
 )
 def test_every_schedule_matches_oracle(orc, monkeypatch, schedule, hidden, C, E):
-    """The three kernel schedules (resident weights / tile ping-pong / N-half
-    pipelined split) give identical, oracle-exact results, including odd
+    """The kernel schedules (two resident-weight jobs in flight / resident
+    weights / tile ping-pong / N-half pipelined split) give identical, oracle-exact results, including odd
     K-chunk splits (96, 160) and layers wider than the previous one."""
     monkeypatch.setenv("BIDA_MLP_FORCE_MODE", schedule)
     blob = make_bmlp1("rc", hidden=hidden, classes=C, ensemble=E, seed=len(hidden) * 100 + C)
@@ -154,3 +154,30 @@ def test_cluster_multicast_on_and_off(orc, monkeypatch, multicast, schedule, hid
     for n in (1001, 148 * 128 * 2 + 77):
         packed = bida.random_walks("rc", n, 0, 30, seed=n)
         check(orc, RC, blob, 0.5, packed, 1, 21)
+
+
+@pytest.mark.parametrize("hidden,C,E", [([128, 128], 21, 1), ([32], 7, 3), ([64, 96, 128], 32, 1)])
+@pytest.mark.parametrize("n", [148 * 128 * 3 + 5, 148 * 128 * 4, 300])
+def test_duo_schedule_many_tiles(orc, monkeypatch, hidden, C, E, n):
+    """Two slots per CTA: odd/even local tile counts, a ragged last tile,
+    CTAs with a single tile, ensembles re-encoding the same tile per member."""
+    monkeypatch.setenv("BIDA_MLP_FORCE_MODE", "duo")
+    blob = make_bmlp1("rc", hidden=hidden, classes=C, ensemble=E, seed=n % 1000 + C)
+    packed = bida.random_walks("rc", n, 0, 30, seed=n)
+    check(orc, RC, blob, 0.5, packed, E, C)
+
+
+@pytest.mark.parametrize(
+    "hidden,C,E,q,ctas",
+    [([1610, 1610], 21, 1, 0.5, 3), ([600], 27, 2, 0.3, 2), ([1024, 2048, 64], 40, 1, 0.5, 5),
+     ([33, 700], 7, 3, 0.9, 1), ([512, 512], 21, 1, 0.5, 148)],
+)
+def test_wide_schedule_matches_oracle(orc, monkeypatch, hidden, C, E, q, ctas):
+    """Wide hidden layers (the paper's 13.6 MB anchor, H = 1610, and widths that
+    are not multiples of the 512-column chunk or of 32): activations round-trip
+    through the per-CTA global scratch.  Few CTAs -> many tiles per CTA."""
+    monkeypatch.setenv("BIDA_MLP_MAX_CTAS", str(ctas))
+    blob = make_bmlp1("rc", hidden=hidden, classes=C, ensemble=E, seed=sum(hidden) + C)
+    packed = bida.random_walks("rc", 128 * 7 + 45 if ctas < 148 else 2000, 0, 30, seed=C)
+    h = check(orc, RC, blob, q, packed, E, C)
+    assert len(np.unique(h)) > 1

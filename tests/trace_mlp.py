@@ -16,6 +16,7 @@ from paper_2507_11916_b200.models import make_bmlp1  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--hidden", default="128,128")
 ap.add_argument("--tiles-per-cta", type=int, default=8)
+ap.add_argument("--warps", default="1,2,6")
 a = ap.parse_args()
 hidden = [int(x) for x in a.hidden.split(",")]
 n = 148 * 128 * a.tiles_per_cta
@@ -24,17 +25,17 @@ d_in = torch.from_numpy(packed.view(np.uint8).copy()).cuda()
 d_h = torch.empty(n, dtype=torch.int32, device="cuda")
 be = bida.MlpModelBackend("rc", make_bmlp1("rc", hidden=hidden, classes=21, seed=3), 0.5)
 slots = _native.lib().bida_gpu_trace_slots()
-buf = torch.zeros(10 * slots, dtype=torch.int64, device="cuda")
+buf = torch.zeros(32 * slots, dtype=torch.int64, device="cuda")
 be.evaluate_device(d_in, d_h)  # warm
 torch.cuda.synchronize()
 _native.check(_native.lib().bida_gpu_debug_trace(be._h, C.c_void_p(buf.data_ptr())))
 be.evaluate_device(d_in, d_h)
 torch.cuda.synchronize()
-t = buf.cpu().numpy().reshape(10, slots)
+t = buf.cpu().numpy().reshape(32, slots)
 t0 = min(int(x) >> 8 for x in t.ravel() if x)
 names = {10: "mma wait act L", 20: "mma got act L", 30: "mma commit L", 40: "epi encode", 41: "epi enc done",
          50: "epi wait d L", 60: "epi got d L", 70: "epi hidden done L", 80: "epi readout done"}
-for w in [1, 2, 6]:
+for w in [int(x) for x in a.warps.split(",")]:
     print(f"--- warp {w}")
     for x in t[w]:
         if not x:
