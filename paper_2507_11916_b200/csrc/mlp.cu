@@ -81,6 +81,7 @@ struct MlpParams {
     PdbArgs pdb;        // optional PDB correction (pdb.cuh)
     uint8_t *scratch;   // wide: per-CTA hidden activations, 2 buffers of sbytes (global, L2-resident)
     long long sbytes;
+    int stage_bytes;    // wide: bytes per weight/activation stage
 };
 
 constexpr int kTraceSlots = 256;
@@ -922,18 +923,31 @@ __global__ void __launch_bounds__(kDuoThreads, 1) mlp_duo_kernel(const __grid_co
 
 // ------------------------------------------------------------------ wide schedule
 // kWide: hidden layers of any width up to kMaxHidden.  A tile's activations
-// no longer fit in shared memory (128 x 1664 B = 208 KB for the paper's
+// no longer fit in shared memory (128 x 1632 B = 204 KB for the paper's
 // 13.6 MB model), so every layer l >= 1 streams its A operand from a per-CTA
 // global scratch buffer (L2-resident, written by the previous layer's
-// epilogue in the UMMA core-matrix layout) together with the weights: a stage
-// is one 32-byte K step = [A 128x32 B][B chunk x 32 B].  Output columns are
-// produced in chunks of 512 (two N <= 256 MMAs into TMEM columns [0,256) and
-// [256,512)); epilogue group g drains half g of each chunk.  Layer 0 reads the
-// one-hot tile X from shared memory, as in the other schedules.
-constexpr int kWideChunk = 512;
-constexpr int kWideStageA = 128 * kKChunk;                   // 4 KB
-constexpr int kWideStage = kWideStageA + kWideChunk * kKChunk;  // 20 KB
-constexpr int kWideMaxStages = 10;
+// epilogue in the UMMA core-matrix layout) together with the weights.
+// Output columns are produced in chunks of 256 (one N <= 256 MMA per 32-byte
+// K step) into two TMEM buffers, so the epilogue drains chunk c (both groups,
+// half the columns each) while the MMAs of chunk c+1 run.  A stage carries ks
+// consecutive K steps, [A ks x 4 KB][B ks x chunk x 32 B], so the issuer's
+// per-stage cost (barrier wait, commit) is amortised over ks MMAs.  Layer 0
+// reads the one-hot tile X from shared memory, as in the other schedules.
+//
+// PAIR (default): CTA pairs run M = 256 MMAs (tcgen05 cta_group::2): each CTA
+// holds its own tile's A rows and HALF of every weight chunk, so the weight
+// bytes each SM pulls from L2 per state halve.  The even CTA issues the MMAs;
+// the odd CTA's idle MMA warp relays its local "stage full" (st.async), "TMEM
+// drained" and "one-hot written" events to the even CTA.
+constexpr int kWideChunk = 256;
+constexpr int kWideStageA = 128 * kKChunk;  // 4 KB of A per K step
+constexpr int kWideMaxStages = 16;
+
+// K steps per stage of a chunk (producer, issuer and relay agree on it).
+__device__ __forceinline__ int wide_ks(int l, int cw, int ns, int nk, int stage_bytes) {
+    const int kb = (l > 0 ? kWideStageA : 0) + cw / ns * kKChunk;
+    return max(1, min(nk, stage_bytes / kb));
+}
 
 // Hidden-layer epilogue into global scratch: TMEM columns [t0, t0 + n) hold
 // output columns [o0, o0 + n) of this thread's row.
@@ -976,41 +990,63 @@ __device__ __forceinline__ void requant_to_global(uint32_t t_row, int t0, const 
     }
 }
 
-template <int DOMAIN, int CM>
+template <int DOMAIN, int CM, bool PAIR>
 __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_constant__ MlpParams p) {
     using T = DomainTraits<DOMAIN>;
+    constexpr int NS = PAIR ? 2 : 1;  // CTAs sharing one weight chunk
     extern __shared__ __align__(1024) uint8_t smem[];
+    const int stage_bytes = p.stage_bytes;
     uint8_t *stages = smem + p.xbytes;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(stages + p.stages * kWideStage);
-    uint64_t *full = bars;                        // [kWideMaxStages]
-    uint64_t *empty = bars + kWideMaxStages;      // [kWideMaxStages]
-    uint64_t *x_ready = bars + 2 * kWideMaxStages;  // one-hot of the tile written (group 1)
-    uint64_t *d_full = x_ready + 1;               // chunk accumulator complete (commit)
-    uint64_t *tmem_free = d_full + 1;             // chunk drained (256 epilogue threads)
-    uint64_t *act_done = tmem_free + 1;           // hidden layer written to scratch (256)
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(act_done + 1);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stages + p.stages * stage_bytes);
+    uint64_t *full = bars;                          // [kWideMaxStages] local TMA landed
+    uint64_t *empty = bars + kWideMaxStages;        // [kWideMaxStages] pair's MMAs done with the stage
+    uint64_t *full2 = bars + 2 * kWideMaxStages;    // [kWideMaxStages] PAIR, even CTA: peer's stage landed
+    uint64_t *x_ready = bars + 3 * kWideMaxStages;  // one-hot of the tile written (group 1)
+    uint64_t *d_full = x_ready + 1;                 // [2] TMEM buffer's chunk complete (commit)
+    uint64_t *tmem_free = d_full + 2;               // [2] TMEM buffer drained (256 epilogue threads)
+    uint64_t *act_done = tmem_free + 2;             // hidden layer written to scratch (256)
+    uint64_t *x_ready2 = act_done + 1;              // PAIR, even CTA: peer's one-hot written
+    uint64_t *tmem_free2 = x_ready2 + 1;            // [2] PAIR, even CTA: peer's buffer drained
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_free2 + 2);
+    uint32_t *sink = tmem_slot + 1;                 // PAIR, even CTA: target of the peer's st.async signals
 
     const int warp = threadIdx.x >> 5;
+    const uint32_t rank = PAIR ? sm100::cluster_rank() : 0u;
     const long long ntiles = (p.n + kTileM - 1) / kTileM;
-    const long long nloc =
-        blockIdx.x < ntiles ? (ntiles - static_cast<long long>(blockIdx.x) + gridDim.x - 1) / gridDim.x : 0;
+    // tile of local iteration kk: CTA pairs take consecutive tile pairs, so both
+    // CTAs of a pair run the same iterations (the odd CTA's may be empty)
+    const long long unit = PAIR ? (blockIdx.x >> 1) : blockIdx.x, nunits = PAIR ? (gridDim.x >> 1) : gridDim.x;
+    const long long nu = PAIR ? (ntiles + 1) / 2 : ntiles;
+    const long long nloc = unit < nu ? (nu - unit + nunits - 1) / nunits : 0;
+    auto tile_of = [&](long long kk) { return PAIR ? 2 * (unit + kk * nunits) + rank : unit + kk * nunits; };
     uint8_t *scr = p.scratch + static_cast<long long>(blockIdx.x) * 2 * p.sbytes;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kWideMaxStages; ++s) {
             sm100::mbar_init(&full[s], 1);
             sm100::mbar_init(&empty[s], 1);
+            sm100::mbar_init(&full2[s], 1);
         }
         sm100::mbar_init(x_ready, 128);
-        sm100::mbar_init(d_full, 1);
-        sm100::mbar_init(tmem_free, 256);
+        for (int b = 0; b < 2; ++b) {
+            sm100::mbar_init(&d_full[b], 1);
+            sm100::mbar_init(&tmem_free[b], 256);
+            sm100::mbar_init(&tmem_free2[b], 1);
+        }
         sm100::mbar_init(act_done, 256);
+        sm100::mbar_init(x_ready2, 1);
         sm100::fence_barrier_init();
     }
-    if (warp == 1)
-        sm100::tmem_alloc(tmem_slot, 512);
+    if (warp == 1) {
+        if constexpr (PAIR)
+            sm100::tmem_alloc_pair(tmem_slot, 512);
+        else
+            sm100::tmem_alloc(tmem_slot, 512);
+    }
     sm100::tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR)
+        sm100::cluster_sync();  // peer barriers initialised before any remote arrive / multicast commit
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     Tracer tr;
@@ -1018,7 +1054,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
         tr.buf = p.trace + static_cast<long long>(warp) * kTraceSlots;
 
     if (warp == 0) {
-        // ------------------------------------------------ producer: [A k-step][B chunk k-step] stages
+        // ------------------------------------------------ producer: [A ks x 4 KB][B ks x chunk part] stages
         if (lane_id() == 0 && nloc > 0) {
             int s = 0;
             uint32_t ph = 0, adph = 0;
@@ -1034,14 +1070,22 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
                         }
                         for (int c0 = 0; c0 < ly.N; c0 += kWideChunk) {
                             const int cw = min(kWideChunk, ly.N - c0);
-                            const uint8_t *b_src = p.wimg + ly.woff + static_cast<long long>(c0) * ly.K;
-                            for (int kc = 0; kc < nk; ++kc) {
+                            const int bb = cw / NS * kKChunk;  // this CTA's B bytes per K step
+                            const int ks = wide_ks(l, cw, NS, nk, stage_bytes);
+                            const uint8_t *b_src =
+                                p.wimg + ly.woff + static_cast<long long>(c0) * ly.K + static_cast<long long>(rank) * bb / kKChunk * ly.K;
+                            for (int kc = 0; kc < nk; kc += ks) {
+                                const int kn = min(ks, nk - kc);
                                 sm100::mbar_wait(&empty[s], ph ^ 1u);
-                                uint8_t *st = stages + s * kWideStage;
-                                sm100::mbar_arrive_expect_tx(&full[s], (l > 0 ? kWideStageA : 0) + cw * kKChunk);
+                                uint8_t *st = stages + s * stage_bytes;
+                                const int abytes = l > 0 ? kn * kWideStageA : 0;
+                                sm100::mbar_arrive_expect_tx(&full[s], abytes + kn * bb);
+                                if (PAIR && rank == 0)  // the peer relay's st.async signal for this stage
+                                    sm100::mbar_arrive_expect_tx(&full2[s], 4u);
                                 if (l > 0)
-                                    sm100::bulk_g2s(st, a_src + kc * kWideStageA, kWideStageA, &full[s]);
-                                sm100::bulk_g2s(st + kWideStageA, b_src + kc * cw * kKChunk, cw * kKChunk, &full[s]);
+                                    sm100::bulk_g2s(st, a_src + kc * kWideStageA, abytes, &full[s]);
+                                sm100::bulk_g2s(st + (l > 0 ? ks * kWideStageA : 0), b_src + static_cast<long long>(kc) * bb,
+                                                kn * bb, &full[s]);
                                 if (++s == p.stages) {
                                     s = 0;
                                     ph ^= 1u;
@@ -1050,12 +1094,49 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
                         }
                     }
         }
+    } else if (warp == 1 && rank == 1) {
+        // ------------------------------------------------ PAIR odd CTA: relay local events to the even CTA,
+        // in the order its MMA issuer consumes them
+        if (lane_id() == 0 && nloc > 0) {
+            const uint32_t r_full2 = sm100::mapa_shared(full2, 0), r_x2 = sm100::mapa_shared(x_ready2, 0),
+                           r_tf2 = sm100::mapa_shared(tmem_free2, 0), r_sink = sm100::mapa_shared(sink, 0);
+            int s = 0;
+            uint32_t ph = 0, xph = 0, cidx = 0;
+            for (long long k = 0; k < nloc; ++k)
+                for (int e = 0; e < p.E; ++e)
+                    for (int l = 0; l < p.nl; ++l) {
+                        const MlpLayer &ly = p.layer[e][l];
+                        const int nk = ly.K / kKChunk;
+                        if (l == 0 && e == 0) {
+                            sm100::mbar_wait(x_ready, xph);
+                            xph ^= 1u;
+                            sm100::mbar_arrive_cluster_relaxed(r_x2);
+                        }
+                        for (int c0 = 0; c0 < ly.N; c0 += kWideChunk, ++cidx) {
+                            const int cw = min(kWideChunk, ly.N - c0);
+                            const int ks = wide_ks(l, cw, NS, nk, stage_bytes);
+                            for (int kc = 0; kc < nk; kc += ks) {
+                                sm100::mbar_wait(&full[s], ph);
+                                sm100::st_async_signal(r_sink, 1u, r_full2 + s * 8u);  // no round-trip wait
+                                if (++s == p.stages) {
+                                    s = 0;
+                                    ph ^= 1u;
+                                }
+                            }
+                            const uint32_t b = cidx & 1u;
+                            sm100::mbar_wait(&tmem_free[b], (cidx >> 1) & 1u);  // this chunk drained here
+                            sm100::mbar_arrive_cluster_relaxed(r_tf2 + b * 8u);
+                        }
+                    }
+        }
     } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer
+        // ------------------------------------------------ MMA issuer (even CTA of a pair)
         if (nloc > 0) {
             int s = 0;
-            uint32_t ph = 0, xph = 0, tfph = 0;
+            uint32_t ph = 0, xph = 0, cidx = 0;
             const uint32_t sX = sm100::smem_u32(smem), sS = sm100::smem_u32(stages);
+            const uint64_t sdelta = static_cast<uint64_t>(stage_bytes) >> 4;
+            uint64_t soff = 0;  // descriptor offset of stage s
             for (long long k = 0; k < nloc; ++k)
                 for (int e = 0; e < p.E; ++e)
                     for (int l = 0; l < p.nl; ++l) {
@@ -1065,59 +1146,90 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
                             if (lane_id() == 0)
                                 tr(10);
                             sm100::mbar_wait(x_ready, xph);
+                            if constexpr (PAIR)
+                                sm100::mbar_wait(x_ready2, xph);
                             xph ^= 1u;
                         }
-                        for (int c0 = 0; c0 < ly.N; c0 += kWideChunk) {
+                        for (int c0 = 0; c0 < ly.N; c0 += kWideChunk, ++cidx) {
                             const int cw = min(kWideChunk, ly.N - c0);
-                            const int w0 = min(256, cw), w1 = cw - w0;
-                            const uint32_t id0 = sm100::make_idesc_i8(w0), id1 = sm100::make_idesc_i8(w1 > 0 ? w1 : 16);
-                            sm100::mbar_wait(tmem_free, tfph ^ 1u);  // previous chunk drained
-                            tfph ^= 1u;
+                            const int ks = wide_ks(l, cw, NS, nk, stage_bytes);
+                            const uint32_t b = cidx & 1u, idesc = sm100::make_idesc_i8(cw, 128u * NS);
+                            const uint32_t dcol = tmem + b * 256u;
+                            sm100::mbar_wait(&tmem_free[b], ((cidx >> 1) & 1u) ^ 1u);  // chunk cidx-2 drained
+                            if constexpr (PAIR)
+                                sm100::mbar_wait(&tmem_free2[b], ((cidx >> 1) & 1u) ^ 1u);
                             if (lane_id() == 0)
                                 tr(20 + l);
                             sm100::tc_fence_after();
-                            uint64_t xdesc = sm100::make_smem_desc(sX, 2048u, 128u);
-                            for (int kc = 0; kc < nk; ++kc) {
+                            // descriptors advanced by adds (no per-step address math on the issue path)
+                            const uint32_t bb = cw / NS * kKChunk;
+                            const uint64_t a0 = sm100::make_smem_desc(sS, 2048u, 128u);
+                            const uint64_t b0 = sm100::make_smem_desc(sS + (l > 0 ? ks * kWideStageA : 0), bb >> 1, 128u);
+                            uint64_t xd = sm100::make_smem_desc(sX, 2048u, 128u);
+                            long long wsum = 0;  // debug timeline: cycles spent waiting for stages
+                            for (int kc = 0; kc < nk; kc += ks) {
+                                const int kn = min(ks, nk - kc);
+                                const long long tw0 = tr.buf ? clock64() : 0;
                                 sm100::mbar_wait(&full[s], ph);
+                                if constexpr (PAIR)
+                                    sm100::mbar_wait(&full2[s], ph);
+                                if (tr.buf)
+                                    wsum += clock64() - tw0;
                                 sm100::tc_fence_after();
-                                const uint32_t st = sS + s * kWideStage;
-                                const uint64_t adesc = l == 0 ? xdesc : sm100::make_smem_desc(st, 2048u, 128u);
-                                const uint64_t b0 = sm100::make_smem_desc(st + kWideStageA, w0 * 16u, 128u);
-                                const uint64_t b1 = sm100::make_smem_desc(st + kWideStageA + w0 * kKChunk, w1 * 16u, 128u);
+                                uint64_t ad = l == 0 ? xd : a0 + soff, bd = b0 + soff;
                                 if (sm100::elect_one()) {
-                                    sm100::mma_i8(tmem, adesc, b0, id0, kc > 0 ? 1u : 0u);
-                                    if (w1 > 0)
-                                        sm100::mma_i8(tmem + 256, adesc, b1, id1, kc > 0 ? 1u : 0u);
-                                    sm100::mma_commit(&empty[s]);
+                                    for (int j = 0; j < kn; ++j) {
+                                        const uint32_t acc = (kc + j) > 0 ? 1u : 0u;
+                                        if constexpr (PAIR)
+                                            sm100::mma_i8_pair(dcol, ad, bd, idesc, acc);
+                                        else
+                                            sm100::mma_i8(dcol, ad, bd, idesc, acc);
+                                        ad += kWideStageA >> 4;
+                                        bd += bb >> 4;
+                                    }
+                                    if constexpr (PAIR)
+                                        sm100::mma_commit_pair(&empty[s]);
+                                    else
+                                        sm100::mma_commit(&empty[s]);
                                 }
                                 __syncwarp();
-                                xdesc += 4096u >> 4;
+                                xd += static_cast<uint64_t>(kn) * (kWideStageA >> 4);
+                                soff += sdelta;
                                 if (++s == p.stages) {
                                     s = 0;
+                                    soff = 0;
                                     ph ^= 1u;
                                 }
                             }
-                            if (sm100::elect_one())
-                                sm100::mma_commit(d_full);
+                            if (sm100::elect_one()) {
+                                if constexpr (PAIR)
+                                    sm100::mma_commit_pair(&d_full[b]);
+                                else
+                                    sm100::mma_commit(&d_full[b]);
+                            }
                             __syncwarp();
-                            if (lane_id() == 0)
+                            if (lane_id() == 0) {
                                 tr(30 + l);
+                                if (tr.buf && tr.n < kTraceSlots)
+                                    tr.buf[tr.n++] = (wsum << 8) | 90;  // value, not a timestamp
+                            }
                         }
                     }
         }
     } else {
         // ------------------------------------------------ encode / epilogue / readout
-        const int grp = (warp - 2) >> 2;  // drains TMEM half grp of every chunk
+        const int grp = (warp - 2) >> 2;  // drains half grp of every chunk's columns
         const int quad = warp & 3;
         const int row = quad * 32 + lane_id();
         const uint32_t sX = sm100::smem_u32(smem);
-        const uint32_t t_row = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-        uint32_t dph = 0;
+        const uint32_t t_row0 = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+        uint32_t cidx = 0;
         const bool reader = grp == 0, encoder = grp == 1;
 
+        auto state_of = [&](long long kk) { return tile_of(kk) * kTileM + row; };
         auto load_state = [&](long long kk, uint64_t &lo_, uint64_t &hi_) {
             lo_ = hi_ = 0;
-            const long long s_ = (blockIdx.x + kk * gridDim.x) * kTileM + row;
+            const long long s_ = state_of(kk);
             if (kk < nloc && s_ < p.n) {
                 if constexpr (T::PB == 16) {
                     const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2 *>(p.packed) + s_);
@@ -1129,15 +1241,15 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
             }
         };
         auto state_bad = [&](uint64_t lo_, uint64_t hi_) {
-            bool b = false;
+            bool bd = false;
 #pragma unroll
             for (int q = 0; q < T::NNZ; ++q) {
                 const int j = position_feature<DOMAIN>(lo_, hi_, q);
-                b |= j < 0 || j >= T::F;
+                bd |= j < 0 || j >= T::F;
             }
-            return b;
+            return bd;
         };
-        auto tile_valid = [&](long long kk) { return kk < nloc && (blockIdx.x + kk * gridDim.x) * kTileM + row < p.n; };
+        auto tile_valid = [&](long long kk) { return kk < nloc && state_of(kk) < p.n; };
         const int nchunk16 = p.Fpad / 16;
         auto encode = [&](uint64_t lo_, uint64_t hi_, bool live_) {
             tr(40);
@@ -1160,7 +1272,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
         if (encoder && nloc > 0)
             encode(nlo, nhi, tile_valid(0) && !state_bad(nlo, nhi));
         for (long long k = 0; k < nloc; ++k) {
-            const long long st = (blockIdx.x + k * gridDim.x) * kTileM + row;
+            const long long st = state_of(k);
             const bool valid = st < p.n;
             const uint64_t lo = nlo, hi = nhi;
             load_state(k + 1, nlo, nhi);
@@ -1177,27 +1289,26 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
                     const int32_t *bias = p.bias + ly.boff;
                     const bool hidden = l + 1 < p.nl;
                     uint8_t *out = scr + (l & 1) * p.sbytes;
-                    for (int c0 = 0; c0 < ly.N; c0 += kWideChunk) {
+                    for (int c0 = 0; c0 < ly.N; c0 += kWideChunk, ++cidx) {
                         const int cw = min(kWideChunk, ly.N - c0);
-                        const int w0 = min(256, cw);
+                        const uint32_t b = cidx & 1u;
+                        const uint32_t t_row = t_row0 + b * 256u;
                         tr(50 + l);
-                        sm100::mbar_wait(d_full, dph);
-                        dph ^= 1u;
+                        sm100::mbar_wait(&d_full[b], (cidx >> 1) & 1u);
                         tr(60 + l);
                         sm100::tc_fence_after();
                         if (hidden) {
-                            const int t0 = grp ? 256 : 0, n = grp ? cw - w0 : w0;
-                            if (n > 0)
-                                requant_to_global(t_row, t0, bias, c0 + t0, n, ly.shift, out, row);
+                            const int half = cw >> 1;  // multiple of 16: widths are padded to 32
+                            requant_to_global(t_row, grp * half, bias, c0 + grp * half, half, ly.shift, out, row);
                             sm100::tc_fence_before();
-                            sm100::mbar_arrive(tmem_free);
+                            sm100::mbar_arrive(&tmem_free[b]);
                             tr(70 + l);
                             continue;
                         }
-                        // output layer (one chunk, C <= 256 columns in half 0)
+                        // output layer (one chunk: C <= 256)
                         if (!reader) {
                             sm100::tc_fence_before();
-                            sm100::mbar_arrive(tmem_free);
+                            sm100::mbar_arrive(&tmem_free[b]);
                             continue;
                         }
                         int32_t v[CM];
@@ -1221,7 +1332,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
                             }
                         }
                         sm100::tc_fence_before();
-                        sm100::mbar_arrive(tmem_free);
+                        sm100::mbar_arrive(&tmem_free[b]);
                         if (p.logits_out && valid) {
                             double *dst = p.logits_out + (static_cast<size_t>(st) * p.E + e) * p.C;
                             for (int c = 0; c < p.C; ++c)
@@ -1260,9 +1371,15 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
     __syncwarp();
     sm100::tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR)
+        sm100::cluster_sync();  // no remote arrive or multicast commit may target an exited CTA
     sm100::tc_fence_after();
-    if (warp == 1)
-        sm100::tmem_dealloc(tmem, 512);
+    if (warp == 1) {
+        if constexpr (PAIR)
+            sm100::tmem_dealloc_pair(tmem, 512);
+        else
+            sm100::tmem_dealloc(tmem, 512);
+    }
 }
 
 // ------------------------------------------------------------------ host
@@ -1280,7 +1397,8 @@ uint32_t rd32(const unsigned char *b) {
 
 template <int DOMAIN, int CM>
 int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
-    auto kern = p.mode == kWide ? mlp_wide_kernel<DOMAIN, CM> : mlp_fused_kernel<DOMAIN, CM>;
+    auto kern = p.mode != kWide ? mlp_fused_kernel<DOMAIN, CM>
+                : (p.cluster == 2 ? mlp_wide_kernel<DOMAIN, CM, true> : mlp_wide_kernel<DOMAIN, CM, false>);
     int threads = kMlpThreads;
     if constexpr (CM == 32) {  // the duo schedule is built for C <= 32 (register budget at 544 threads)
         if (p.mode == kDuo) {
@@ -1296,6 +1414,8 @@ int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
     }
     const long long ntiles = (p.n + kTileM - 1) / kTileM;
     int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(ntiles, m->grid_cap)));
+    if (p.cluster == 2)
+        grid = (grid + 1) & ~1;
     MlpParams q = p;
     if (p.mode == kWide) {  // per-launch scratch from the stream-ordered pool (concurrent launches are safe)
         e = cudaMallocAsync(reinterpret_cast<void **>(&q.scratch), static_cast<size_t>(grid) * 2 * p.sbytes, st);
@@ -1305,7 +1425,6 @@ int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
         }
     }
     if (p.cluster == 2) {
-        grid = (grid + 1) & ~1;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(kMlpThreads);
@@ -1375,7 +1494,7 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     std::vector<int> Hp(L);  // widths padded to the 32-byte MMA K step (zero weights and bias)
     for (uint32_t l = 0; l < L; ++l)
         Hp[l] = (H[l] + 31) / 32 * 32;
-    const int Cpad = std::max(16, (static_cast<int>(C) + 15) / 16 * 16);
+    const int Cpad = (static_cast<int>(C) + 31) / 32 * 32;  // N of the output MMA: a multiple of 32 (CTA pairs)
     const int nl = static_cast<int>(L) + 1;
     auto *m = new MlpModel();
     MlpParams &p = m->p;
@@ -1498,12 +1617,18 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     const bool fit_pair = Nmax <= 256 && stages_for(2 * set1) >= 2;
     const bool want_split = fm == "split" && stages_for(set1) >= 2;
     const bool fit_split = Nmax <= 512 && stages_for(set1) >= 2;
-    const size_t wide_bars = 8 * (2 * kWideMaxStages + 4) + 16;
+    // wide: CTA pairs (M = 256 MMAs, half of every weight chunk per CTA) only with
+    // BIDA_MLP_WIDE_PAIR=1: measured slower than one CTA per tile (profiles/r1_notes.md)
+    const char *wpv = std::getenv("BIDA_MLP_WIDE_PAIR");
+    const bool wide_pair = wpv && wpv[0] == '1';
+    // a stage holds 3 K steps of a full chunk: [A 3 x 4 KB][B 3 x 256 x 32 B (/2 per CTA of a pair)]
+    const int wide_stage = 3 * (kWideStageA + kWideChunk * kKChunk / (wide_pair ? 2 : 1));
+    const size_t wide_bars = 8 * (3 * kWideMaxStages + 9) + 16;
     const size_t xwide = static_cast<size_t>(kTileM) * Fpad;
     const int wide_stages =
-        xwide + wide_bars + 2 * kWideStage > budget
+        xwide + wide_bars + 2 * wide_stage > budget
             ? 0
-            : static_cast<int>(std::min<size_t>(kWideMaxStages, (budget - xwide - wide_bars) / kWideStage));
+            : static_cast<int>(std::min<size_t>(kWideMaxStages, (budget - xwide - wide_bars) / wide_stage));
     if (wide_stages >= 2 && (fm == "wide" || Nmax > 512 || (!fit_res && !fit_pair && !fit_split))) {
         p.mode = kWide;
         p.stages = wide_stages;
@@ -1511,7 +1636,9 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
         p.ybytes = 0;
         p.tmem_cols = 512u;
         p.sbytes = static_cast<long long>(kTileM) * Kmax;
-        m->smem = xwide + static_cast<size_t>(wide_stages) * kWideStage + wide_bars;
+        p.stage_bytes = wide_stage;
+        p.cluster = wide_pair ? 2 : 1;
+        m->smem = xwide + static_cast<size_t>(wide_stages) * wide_stage + wide_bars;
     } else if (fit_duo && fm == "duo") {  // two jobs in flight, resident weights (opt-in: see r1_notes.md)
         p.mode = kDuo;
         p.stages = 0;
@@ -1554,23 +1681,23 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
                     ly.nh = 1;
                     ly.cps = 1;
                     ly.woff = static_cast<long long>(pos0);
+                    // chunks of <= 256 output columns; a chunk is NS parts (CTA r of a pair
+                    // holds rows [r*cw/2, (r+1)*cw/2)), each K/32 consecutive steps of
+                    // rows x 32 B in the core-matrix layout (a stage loads ks steps at once)
+                    const int ns = p.cluster == 2 ? 2 : 1;
                     for (int c0 = 0; c0 < ly.N; c0 += kWideChunk) {
-                        const int cw = std::min(kWideChunk, ly.N - c0), w0 = std::min(256, cw), w1 = cw - w0;
-                        for (int kc = 0; kc < ly.K / 32; ++kc) {
-                            const size_t base = pos0 + static_cast<size_t>(c0) * ly.K + static_cast<size_t>(kc) * cw * 32;
-                            for (int nn = 0; nn < cw; ++nn) {
-                                const int n = c0 + nn;
-                                if (n >= w.outn)
-                                    continue;
-                                const bool h1 = nn >= w0;
-                                const int hw = h1 ? w1 : w0, r = h1 ? nn - w0 : nn;
-                                for (int k = 0; k < 32; ++k) {
-                                    const int kk = kc * 32 + k;
-                                    if (kk >= w.in)
-                                        continue;
-                                    img[base + (h1 ? w0 * 32 : 0) + (k / 16) * (hw * 16) + (r / 8) * 128 + (r % 8) * 16 +
-                                        (k % 16)] = static_cast<uint8_t>(w.W[static_cast<size_t>(n) * w.in + kk]);
-                                }
+                        const int cw = std::min(kWideChunk, ly.N - c0), rows = cw / ns;
+                        for (int nn = 0; nn < cw; ++nn) {
+                            const int n = c0 + nn;
+                            if (n >= w.outn)
+                                continue;
+                            const int part = nn / rows, r = nn % rows;
+                            for (int kk = 0; kk < w.in; ++kk) {
+                                const int kc = kk / 32, k = kk % 32;
+                                const size_t pos = pos0 + static_cast<size_t>(c0) * ly.K + static_cast<size_t>(part) * rows * ly.K +
+                                                   static_cast<size_t>(kc) * rows * 32 + (k / 16) * (rows * 16) + (r / 8) * 128 +
+                                                   (r % 8) * 16 + (k % 16);
+                                img[pos] = static_cast<uint8_t>(w.W[static_cast<size_t>(n) * w.in + kk]);
                             }
                         }
                     }
@@ -1604,7 +1731,8 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     // 1.16 vs 1.26 G evals/s) -- the pair's lockstep costs more than the halved
     // per-SM copy issue saves (profiles/r1_notes.md).
     const char *mcv = std::getenv("BIDA_MLP_MULTICAST");
-    p.cluster = ((p.mode == kPair || p.mode == kSplit) && mcv && mcv[0] == '1') ? 2 : 1;
+    if (p.mode != kWide)
+        p.cluster = ((p.mode == kPair || p.mode == kSplit) && mcv && mcv[0] == '1') ? 2 : 1;
     m->cm = C <= 32 ? 32 : (C <= 64 ? 64 : 256);
     m->grid_cap = num_sms;
     if (const char *mc = std::getenv("BIDA_MLP_MAX_CTAS"))  // tests: many tiles per CTA on small batches

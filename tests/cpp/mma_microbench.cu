@@ -131,6 +131,88 @@ __global__ void __launch_bounds__(512, 1) contention(int n_mma, int N, int sts_w
         sm100::tmem_dealloc(tmem, 512);
 }
 
+// Streaming operands: every MMA reads a DIFFERENT A (4 KB) and B (N*32 B) from
+// a ring of `nbuf` operand sets, optionally while warp 1 keeps the TMA engine
+// writing `tma_kb` KB stages from global memory into a separate region (the
+// wide schedule's situation).  Reports cycles per MMA.
+__global__ void __launch_bounds__(128, 1) stream(int n_mma, int N, int nbuf, int tma_kb, const uint8_t *gsrc,
+                                                 long long *out, int commit_every) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar, tbar, cbar;
+    __shared__ uint32_t tslot;
+    __shared__ volatile int stop;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t setb = 4096u + N * 32u;
+    if (threadIdx.x == 0)
+        sm100::mbar_init(&cbar, 1);
+    if (threadIdx.x == 0) {
+        sm100::mbar_init(&bar, 1);
+        sm100::mbar_init(&tbar, 1);
+        sm100::fence_barrier_init();
+        stop = 0;
+    }
+    for (int i = threadIdx.x; i < (int)(nbuf * setb / 16); i += blockDim.x)
+        reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+    sm100::fence_proxy_async_smem();
+    if (warp == 0)
+        sm100::tmem_alloc(&tslot, 512);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = tslot;
+    if (warp == 0) {
+        // whole warp walks the loop, descriptors advanced by adds, elected lane issues
+        const uint32_t base = sm100::smem_u32(smem);
+        const uint32_t idesc = sm100::make_idesc_i8(N);
+        const uint64_t a0 = sm100::make_smem_desc(base, 2048u, 128u);
+        const uint64_t b0 = sm100::make_smem_desc(base + 4096u, N * 16u, 128u);
+        const long long t0 = clock64();
+        uint64_t off = 0;
+        int j = 0;
+        for (int i = 0; i < n_mma; ++i) {
+            if (sm100::elect_one()) {
+                sm100::mma_i8(tmem, a0 + off, b0 + off, idesc, i > 0 ? 1u : 0u);
+                if (commit_every && (i % commit_every) == commit_every - 1)
+                    sm100::mma_commit(&cbar);  // per-stage release, as the streaming schedules do
+            }
+            __syncwarp();
+            off += setb >> 4;
+            if (++j == nbuf) {
+                j = 0;
+                off = 0;
+            }
+        }
+        if (sm100::elect_one())
+            sm100::mma_commit(&bar);
+        __syncwarp();
+        sm100::mbar_wait(&bar, 0);
+        if (threadIdx.x == 0) {
+            out[blockIdx.x] = clock64() - t0;
+            stop = 1;
+        }
+    } else if (warp == 1 && tma_kb > 0) {
+        if (threadIdx.x == 32) {
+            uint8_t *dst = smem + nbuf * setb;
+            uint32_t ph = 0;
+            const uint32_t bytes = tma_kb * 1024u;
+            long long off = (blockIdx.x * 7919LL * 1024) % (64LL << 20);
+            while (!stop) {
+                sm100::mbar_arrive_expect_tx(&tbar, bytes);
+                sm100::bulk_g2s(dst, gsrc + off, bytes, &tbar);
+                sm100::mbar_wait(&tbar, ph);
+                ph ^= 1u;
+                off = (off + bytes) % (64LL << 20);
+            }
+        }
+    }
+    __syncwarp();
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    if (warp == 0)
+        sm100::tmem_dealloc(tmem, 512);
+}
+
 int main() {
     long long *d_out, h_out[2 * 148];
     cudaMalloc(&d_out, sizeof(h_out));
@@ -178,5 +260,33 @@ int main() {
                 printf("contention A=%s N=%3d sts_warps=%2d  %.1f cyc/mma (floor %.0f)\n", ts ? "tmem" : "smem", N, w,
                        tot / n, 128.0 * N / 256.0);
             }
+    {
+        uint8_t *g;
+        cudaMalloc(&g, (64 << 20) + (64 << 10));
+        cudaMemset(g, 1, (64 << 20) + (64 << 10));
+        cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        for (int ce : {0, 1, 2, 4})
+        for (int N : {32, 128, 256})
+            for (int nbuf : {8})
+                for (int tkb : {0}) {
+                    const int n = 2048;
+                    const int setb = 4096 + N * 32;
+                    if (nbuf * setb + tkb * 1024 > 200 * 1024)
+                        continue;
+                    stream<<<148, 128, 200 * 1024>>>(n, N, nbuf, tkb, g, d_out, ce);
+                    cudaError_t e = cudaDeviceSynchronize();
+                    if (e != cudaSuccess) {
+                        printf("error %s\n", cudaGetErrorString(e));
+                        return 1;
+                    }
+                    cudaMemcpy(h_out, d_out, sizeof(long long) * 148, cudaMemcpyDeviceToHost);
+                    double tot = 0;
+                    for (int g2 = 0; g2 < 148; ++g2)
+                        tot += h_out[g2];
+                    tot /= 148;
+                    printf("stream N=%3d operand sets=%d tma_stage=%2d KB commit_every=%d  %.1f cyc/mma (floor %.0f)  smem read %.0f B/clk\n", N,
+                           nbuf, tkb, ce, tot / n, 128.0 * N / 256.0, (4096.0 + N * 32.0) / (tot / n));
+                }
+    }
     return 0;
 }

@@ -172,11 +172,15 @@ def test_duo_schedule_many_tiles(orc, monkeypatch, hidden, C, E, n):
     [([1610, 1610], 21, 1, 0.5, 3), ([600], 27, 2, 0.3, 2), ([1024, 2048, 64], 40, 1, 0.5, 5),
      ([33, 700], 7, 3, 0.9, 1), ([512, 512], 21, 1, 0.5, 148)],
 )
-def test_wide_schedule_matches_oracle(orc, monkeypatch, hidden, C, E, q, ctas):
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_wide_schedule_matches_oracle(orc, monkeypatch, hidden, C, E, q, ctas, pair):
     """Wide hidden layers (the paper's 13.6 MB anchor, H = 1610, and widths that
     are not multiples of the 512-column chunk or of 32): activations round-trip
-    through the per-CTA global scratch.  Few CTAs -> many tiles per CTA."""
+    through the per-CTA global scratch.  Few CTAs -> many tiles per CTA; an odd
+    CTA cap leaves a CTA pair with empty tiles.  pair=1: M = 256 MMAs across a
+    CTA pair (cta_group::2), pair=0: one CTA per tile."""
     monkeypatch.setenv("BIDA_MLP_MAX_CTAS", str(ctas))
+    monkeypatch.setenv("BIDA_MLP_WIDE_PAIR", pair)
     blob = make_bmlp1("rc", hidden=hidden, classes=C, ensemble=E, seed=sum(hidden) + C)
     packed = bida.random_walks("rc", 128 * 7 + 45 if ctas < 148 else 2000, 0, 30, seed=C)
     h = check(orc, RC, blob, q, packed, E, C)

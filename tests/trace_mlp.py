@@ -32,7 +32,7 @@ _native.check(_native.lib().bida_gpu_debug_trace(be._h, C.c_void_p(buf.data_ptr(
 be.evaluate_device(d_in, d_h)
 torch.cuda.synchronize()
 t = buf.cpu().numpy().reshape(32, slots)
-t0 = min(int(x) >> 8 for x in t.ravel() if x)
+t0 = min(int(x) >> 8 for x in t.ravel() if x and (int(x) & 0xFF) != 90)
 names = {10: "mma wait act L", 20: "mma got act L", 30: "mma commit L", 40: "epi encode", 41: "epi enc done",
          50: "epi wait d L", 60: "epi got d L", 70: "epi hidden done L", 80: "epi readout done"}
 for w in [int(x) for x in a.warps.split(",")]:
@@ -42,6 +42,9 @@ for w in [int(x) for x in a.warps.split(",")]:
             break
         tag = int(x) & 0xFF
         base = max(k for k in names if k <= tag)
+        if tag == 90:
+            print(f"{'':9s}  (stage waits in this chunk: {int(x) >> 8} cycles)")
+            continue
         if tag in (81, 82, 83):
             print(f"{(int(x) >> 8) - t0:9d}  readout mark {tag}")
             continue
