@@ -43,6 +43,7 @@ WORKLOADS = {
     "rc-mlp-h1610": dict(domain="rc", kind="mlp", H=[1610, 1610], E=1, C=21, q=0.5, batch=1 << 21),
 }
 DEFAULT_WORKLOAD = "rc-mlp-h128"
+WIDE_WORKLOAD = "rc-mlp-h1610"
 
 PACKED = {"rc": 16, "stp4": 8, "stp3": 8, "stp2": 8}
 NNZ = {"rc": 20, "stp4": 16, "stp3": 9, "stp2": 4}
@@ -186,7 +187,7 @@ def make_backend(wl, device):
     return bida.MlpModelBackend(wl["domain"], blob, wl["q"], device=device)
 
 
-def run_ours(args, wl, rank, world, local):
+def run_ours(args, wl, rank, world, local, e2e=True):
     import torch
 
     import paper_2507_11916_b200 as bida
@@ -229,6 +230,12 @@ def run_ours(args, wl, rank, world, local):
     kern_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms_max = reduce_max(total_ms, world)
     kern_avg_ms = float(np.mean(kern_ms))
+
+    if not e2e:
+        clk.__exit__(None, None, None)
+        be.close()
+        return dict(B=B, nbuf=nbuf, total_ms=total_ms_max, kern_avg_ms=kern_avg_ms, launches=launches,
+                    clocks=clk.summary())
 
     # ---- end-to-end through the C-ABI with host buffers (e2e) ------------
     try:
@@ -396,6 +403,37 @@ def run_reference_arm(args, wl, rank, world):
     }
 
 
+def roofline_for(name, wl, B, kern_avg_ms):
+    """Roofline of the dominant (only) kernel: algorithmic bytes or flops per
+    launch / its CUDA-event time; peaks from MEASURED_PEAKS.json; traffic from
+    the committed ncu capture of this workload (profiles/traffic.json)."""
+    by, fl = algorithmic(wl)
+    peaks = {}
+    pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk_path):
+        peaks = json.load(open(pk_path))
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    kern_s = kern_avg_ms / 1000.0
+    traffic, traffic_src = None, None
+    tj = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tj):
+        t = json.load(open(tj)).get(name)
+        if t:
+            traffic = t["bytes_per_launch"] * B / t["states_per_launch"]
+            traffic_src = t["source"]
+    if wl["kind"] == "linear":
+        achieved = by * B / kern_s / 1e9
+        return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+                "algorithmic_bytes_per_state": by}
+    achieved = fl * B / kern_s / 1e12
+    pk = peaks.get("bf16_tflops", 1590.0) * 2  # dense int8 = 2x dense bf16 (see DESIGN.md §5)
+    return {"bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
+            "frac": achieved / pk, "traffic": traffic, "traffic_source": traffic_src, "flops_per_state": fl,
+            "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x dense bf16 on B200)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -407,6 +445,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample size (seconds of work)")
     ap.add_argument("--ref-step-seconds", type=float, default=2.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-wide-leg", dest="wide_leg", action="store_false",
+                    help="skip the config-4 (H=1610) device-resident leg of an N=1 run")
     ap.add_argument("--search-seconds", type=float, default=10.0,
                     help="Batch IDA* nodes/s leg (RC MLP workloads, N=1); 0 disables")
     args = ap.parse_args()
@@ -426,36 +466,7 @@ def main():
     B = r["B"]
     total_states = B * args.steps * world
     value = whole_job_rate(B, args.steps, world, r["total_ms"])
-    by, fl = algorithmic(wl)
-    import json as _json
-
-    peaks = {}
-    pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(pk_path):
-        peaks = _json.load(open(pk_path))
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    kern_s = r["kern_avg_ms"] / 1000.0
-    # DRAM traffic of the dominant kernel per launch, from the committed ncu
-    # --set full capture of this workload (profiles/traffic.json), scaled to B
-    traffic, traffic_src = None, None
-    tj = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tj):
-        t = _json.load(open(tj)).get(args.workload)
-        if t:
-            traffic = t["bytes_per_launch"] * B / t["states_per_launch"]
-            traffic_src = t["source"]
-    if wl["kind"] == "linear":
-        achieved = by * B / kern_s / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-                "algorithmic_bytes_per_state": by}
-    else:
-        achieved = fl * B / kern_s / 1e12
-        pk = peaks.get("bf16_tflops", 1590.0) * 2  # dense int8 = 2x dense bf16
-        roof = {"bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
-                "frac": achieved / pk, "traffic": traffic, "traffic_source": traffic_src, "flops_per_state": fl,
-                "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x dense bf16 on B200)"}
+    roof = roofline_for(args.workload, wl, B, r["kern_avg_ms"])
     line = {
         "metric": "heuristic_evals_per_s",
         "value": value,
@@ -485,6 +496,16 @@ def main():
         "clocks": r["clocks"],
         "kernel_ms_avg": r["kern_avg_ms"],
     }
+    if world == 1 and args.wide_leg and args.workload != WIDE_WORKLOAD:
+        # config 4 (the paper's 13.6 MB model): the tensor-bound case
+        # the north star's tensor-utilisation target refers to; device-resident only
+        ww = WORKLOADS[WIDE_WORKLOAD]
+        rw = run_ours(args, ww, rank, world, local, e2e=False)
+        line["wide_model"] = {
+            "workload": WIDE_WORKLOAD, "model": {k: v for k, v in ww.items() if k in ("kind", "E", "C", "q", "H")},
+            "value": whole_job_rate(rw["B"], args.steps, world, rw["total_ms"]), "unit": "evals/s",
+            "batch_per_gpu": rw["B"], "kernel_ms_avg": rw["kern_avg_ms"], "gpu_launches": int(rw["launches"]),
+            "roofline": roofline_for(WIDE_WORKLOAD, ww, rw["B"], rw["kern_avg_ms"]), "clocks": rw["clocks"]}
     if world == 1 and not args.no_cpu_baseline:
         threads = host_cores()
         run, kind, n = cpu_rate(wl, args.cpu_seconds, threads)

@@ -77,7 +77,10 @@ def lib() -> C.CDLL:
             f"CUDA evaluator library not built: {LIB_PATH} is missing "
             "(run `python -c 'import __graft_entry__ as g; g.build()'`)"
         )
-    L = C.CDLL(LIB_PATH)
+    path = LIB_PATH
+    if os.environ.get("BIDA_GPU_TRACE") == "1":  # diagnostic build with the kernel timeline compiled in
+        path = os.path.join(HERE, "_lib", "libbida_gpu_trace.so")
+    L = C.CDLL(path)
     vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int
     H = C.c_void_p
     L.bida_gpu_abi_version.restype = i32

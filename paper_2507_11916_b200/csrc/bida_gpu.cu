@@ -733,6 +733,10 @@ int bida_gpu_attach_pdb_file(bida_gpu_evaluator *ev, const char *path, int mode)
 int bida_gpu_debug_trace(bida_gpu_evaluator *ev, long long *dev_buf) {
     if (!ev || ev->kind != BIDA_MODEL_MLP)
         return fail(BIDA_ERR_INVALID_ARGUMENT, "debug trace needs an MLP evaluator");
+#if !defined(BIDA_MLP_TRACE) || !BIDA_MLP_TRACE
+    if (dev_buf)
+        return fail(BIDA_ERR_STATE, "tracing is compiled into libbida_gpu_trace.so only (build.py trace=True)");
+#endif
     mlp_set_trace(ev->mlp, dev_buf);
     return BIDA_OK;
 }

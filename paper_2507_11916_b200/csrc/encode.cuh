@@ -52,6 +52,27 @@ struct DomainTraits<kSTP4> { static constexpr int F = 256, NNZ = 16, PB = 8; };
 template <>
 struct DomainTraits<kRC> { static constexpr int F = 480, NNZ = 20, PB = 16; };
 
+// True when some position's feature index falls outside [0, F) -- the same
+// predicate as checking position_feature() for every position.  Rubik's cube:
+// only an edge label >= 12 can leave the range (192 + e*24 + p*2 + eo >= 480
+// iff e >= 12; corner indices stay below 192), i.e. bits 3 and 2 of a hi
+// nibble both set.
+template <int DOMAIN>
+__device__ __forceinline__ bool state_out_of_range(uint64_t lo, uint64_t hi) {
+    if constexpr (DOMAIN == kRC) {
+        return ((hi & (hi << 1)) & 0x888888888888ull) != 0;
+    } else {
+        using T = DomainTraits<DOMAIN>;
+        bool b = false;
+#pragma unroll
+        for (int q = 0; q < T::NNZ; ++q) {
+            const int j = position_feature<DOMAIN>(lo, hi, q);
+            b |= j < 0 || j >= T::F;
+        }
+        return b;
+    }
+}
+
 // Warp-cooperative: writes the ascending unique active indices of one state
 // into sidx[0..count) and returns count.  *bad is set (warp-uniform) when an
 // index falls outside [0, F) — a malformed packed state.

@@ -16,7 +16,10 @@
 //              softmax/quantile (float64 replay when undecidable) -> min
 //              over members -> h
 // Warp roles: warp 0 producer (1 thread), warp 1 MMA issuer (1 thread),
-// warps 2-5 encode/epilogue/readout (thread = TMEM lane = tile row).
+// warps 2-9 two encode/epilogue/readout groups (thread = TMEM lane = tile row).
+// Schedules: resident / pair / split (mlp_fused_kernel, activations in shared
+// memory) and wide (mlp_wide_kernel: hidden layers up to 4096 wide, activations
+// in L2-resident global scratch) -- see the comments at each kernel.
 //
 // Integer arithmetic makes every logit exact, so h is bit-identical to the
 // oracle's BMLP1 restatement (oracle/bida_oracle.c) in any MMA order.
@@ -46,7 +49,7 @@ constexpr int kMaxStages = 6;
 constexpr int kStageBytes = 16384;
 constexpr int kMlpThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2-9 two epilogue groups
 constexpr int kKChunk = 32;       // bytes of K per MMA instruction
-enum MlpMode { kPair = 0, kSplit = 1, kResident = 2, kDuo = 3, kWide = 4 };
+enum MlpMode { kPair = 0, kSplit = 1, kResident = 2, kWide = 4 };
 
 struct MlpLayer {
     int K, N;          // padded input width (multiple of 32), output width (multiple of 16)
@@ -82,6 +85,7 @@ struct MlpParams {
     uint8_t *scratch;   // wide: per-CTA hidden activations, 2 buffers of sbytes (global, L2-resident)
     long long sbytes;
     int stage_bytes;    // wide: bytes per weight/activation stage
+    int bias_bytes;     // wide: whole bias vector staged in shared memory (0: read from global)
 };
 
 constexpr int kTraceSlots = 256;
@@ -105,15 +109,113 @@ thread_local std::string g_err;
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // Debug timeline: lane 0 of each warp of CTA 0 appends (clock64 << 8 | tag).
+// Compiled in only for the diagnostic library (build.py trace=True,
+// -DBIDA_MLP_TRACE=1): the per-call checks cost ~6% of the fused kernel's
+// instructions (profiles/r1_notes.md).
+#ifndef BIDA_MLP_TRACE
+#define BIDA_MLP_TRACE 0
+#endif
 struct Tracer {
+    static constexpr bool kOn = BIDA_MLP_TRACE != 0;
     long long *buf = nullptr;
     int n = 0;
+    __device__ bool on() const { return kOn && buf != nullptr; }
     __device__ void operator()(int tag) {
-        if (buf && n < kTraceSlots)
+        if (on() && n < kTraceSlots)
             buf[n++] = (clock64() << 8) | (tag & 0xFF);
+    }
+    __device__ void value(long long v, int tag) {  // a value instead of a timestamp
+        if (on() && n < kTraceSlots)
+            buf[n++] = (v << 8) | (tag & 0xFF);
     }
 };
 } // namespace
+
+// Hidden-layer epilogue of one thread (= TMEM lane = tile row): TMEM columns
+// [t0, t0 + n) (n a multiple of 16) hold output columns [o0, o0 + n); each is
+// requantised, (acc + bias) >> sh saturated to u8, and stored as the next
+// layer's K-major A operand -- into shared memory at `sout` (GLOBAL = false)
+// or global scratch at `gout` (GLOBAL = true, 4 KB per 32 columns).  The
+// TMEM loads of up to 64 columns are issued back to back and waited for once:
+// a tcgen05.ld round trip costs several hundred cycles, so one wait per 16
+// columns made the drain latency-bound.
+// `bias` (global) or, when bias_s != 0, the same vector staged in shared
+// memory at bias_s (the wide schedule: its L1 is too small to keep it).
+template <bool GLOBAL>
+__device__ __forceinline__ void requant_block(uint32_t t_row, int t0, const int32_t *bias, int o0, int n, int sh,
+                                              uint32_t sout, uint8_t *gout, int row, uint32_t bias_s = 0u) {
+    for (int j = 0; j < n; j += 64) {
+        const int m = min(64, n - j);
+        int32_t r[4][16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (q * 16 < m)
+                sm100::tmem_ld16(t_row + t0 + j + q * 16, r[q]);
+        sm100::tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (q * 16 >= m)
+                break;
+            const int oc = o0 + j + q * 16;
+            int4 b4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                b4[u] = bias_s ? sm100::ld_shared_v4(bias_s + (oc + 4 * u) * 4u)
+                               : __ldg(reinterpret_cast<const int4 *>(bias + oc) + u);
+            uint32_t w[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                w[u] = sm100::pack_sat_u8x4((r[q][u * 4 + 0] + b4[u].x) >> sh, (r[q][u * 4 + 1] + b4[u].y) >> sh,
+                                            (r[q][u * 4 + 2] + b4[u].z) >> sh, (r[q][u * 4 + 3] + b4[u].w) >> sh);
+            if constexpr (GLOBAL)
+                sm100::st_global_v4(gout + (oc >> 5) * 4096 + ((oc >> 4) & 1) * 2048 + row * 16, w[0], w[1], w[2], w[3]);
+            else
+                sm100::st_shared_v4(sout + (oc >> 4) * 2048u + row * 16u, w[0], w[1], w[2], w[3]);
+        }
+    }
+}
+
+// Hidden-layer epilogue into shared memory for the fused schedules (L1-hit
+// bias): the TMEM load of the next 16 columns is in flight while the current
+// 16 are requantised and stored.  Columns [c_beg, c_end) of this thread's row.
+__device__ __forceinline__ void requant_pipelined(uint32_t t_row, const int32_t *bias, int sh, uint32_t out, int row,
+                                                  int c_beg, int c_end) {
+    auto requant = [&](const int32_t(&r)[16], const int4(&b4)[4], int c0) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)  // saturated to u8 0..255
+            w[q] = sm100::pack_sat_u8x4((r[q * 4 + 0] + b4[q].x) >> sh, (r[q * 4 + 1] + b4[q].y) >> sh,
+                                        (r[q * 4 + 2] + b4[q].z) >> sh, (r[q * 4 + 3] + b4[q].w) >> sh);
+        sm100::st_shared_v4(out + (c0 >> 4) * 2048u + row * 16u, w[0], w[1], w[2], w[3]);
+    };
+    auto load_bias = [&](int4(&b4)[4], int c0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
+    };
+    int32_t ra[16], rb[16];
+    int4 ba[4], bb[4];
+    sm100::tmem_ld16(t_row + c_beg, ra);
+    load_bias(ba, c_beg);
+    sm100::tmem_wait_ld();
+    for (int c0 = c_beg; c0 < c_end; c0 += 32) {
+        const bool has_b = c0 + 16 < c_end;
+        if (has_b) {
+            sm100::tmem_ld16(t_row + c0 + 16, rb);
+            load_bias(bb, c0 + 16);
+        }
+        requant(ra, ba, c0);
+        sm100::tmem_wait_ld();
+        if (!has_b)
+            break;
+        if (c0 + 32 < c_end) {
+            sm100::tmem_ld16(t_row + c0 + 32, ra);
+            load_bias(ba, c0 + 32);
+        }
+        requant(rb, bb, c0 + 16);
+        sm100::tmem_wait_ld();
+    }
+}
 
 // One CTA per SM, persistent over the CTA's tiles of 128 states (local tile k
 // of this CTA is t = blockIdx.x + k * gridDim.x).  A "job" is one (tile,
@@ -180,7 +282,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     Tracer tr;
-    if (p.trace && blockIdx.x == 0 && lane_id() == 0)
+    if (Tracer::kOn && p.trace && blockIdx.x == 0 && lane_id() == 0)
         tr.buf = p.trace + static_cast<long long>(warp) * kTraceSlots;
 
     if (warp == 0) {
@@ -410,28 +512,20 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                 }
             }
         };
-        auto state_bad = [&](uint64_t lo_, uint64_t hi_) {
-            bool b = false;
-#pragma unroll
-            for (int q = 0; q < T::NNZ; ++q) {
-                const int j = position_feature<DOMAIN>(lo_, hi_, q);
-                b |= j < 0 || j >= T::F;
-            }
-            return b;
-        };
+        auto state_bad = [&](uint64_t lo_, uint64_t hi_) { return state_out_of_range<DOMAIN>(lo_, hi_); };
         // one-hot row of a packed state into X (layer 0's A operand), then publish
         // (the split schedule's one-hot is written whole by group 1; see below)
-        const int c_lo = 0, c_hi = p.Fpad / 16;
+        constexpr int kX16 = (T::F + 31) / 32 * 2;  // 16-column chunks of the one-hot tile (Fpad / 16)
         auto encode = [&](uint64_t lo_, uint64_t hi_, bool live_, uint64_t *bar) {
             tr(40);
-            for (int c16 = c_lo; c16 < c_hi; ++c16)
+#pragma unroll
+            for (int c16 = 0; c16 < kX16; ++c16)
                 sm100::st_shared_v4(sX + c16 * 2048u + row * 16u, 0u, 0u, 0u, 0u);
             if (live_) {
 #pragma unroll
                 for (int q = 0; q < T::NNZ; ++q) {
                     const int j = position_feature<DOMAIN>(lo_, hi_, q);
-                    if ((j >> 4) >= c_lo && (j >> 4) < c_hi)
-                        sm100::st_shared_u8(sX + (j >> 4) * 2048u + row * 16u + (j & 15), 1u);
+                    sm100::st_shared_u8(sX + (j >> 4) * 2048u + row * 16u + (j & 15), 1u);
                 }
             }
             sm100::fence_proxy_async_smem();
@@ -485,44 +579,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                         const uint32_t out = ((l + 1) & 1) ? sY : sX;
                         const int half = mode == kPair ? ly.N : ly.N / 2;
                         const int c_beg = mode == kPair ? 0 : grp * half, c_end = c_beg + half;
-                        // software-pipelined: the TMEM load of the next 16 columns is in
-                        // flight while the current 16 are requantised and stored
-                        const int sh = ly.shift;
-                        auto requant = [&](const int32_t(&r)[16], const int4(&b4)[4], int c0) {
-                            uint32_t w[4];
-#pragma unroll
-                            for (int q = 0; q < 4; ++q)  // saturated to u8 0..255
-                                w[q] = sm100::pack_sat_u8x4((r[q * 4 + 0] + b4[q].x) >> sh, (r[q * 4 + 1] + b4[q].y) >> sh,
-                                                            (r[q * 4 + 2] + b4[q].z) >> sh, (r[q * 4 + 3] + b4[q].w) >> sh);
-                            sm100::st_shared_v4(out + (c0 >> 4) * 2048u + row * 16u, w[0], w[1], w[2], w[3]);
-                        };
-                        auto load_bias = [&](int4(&b4)[4], int c0) {
-#pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
-                        };
-                        int32_t ra[16], rb[16];
-                        int4 ba[4], bb[4];
-                        sm100::tmem_ld16(t_row + c_beg, ra);
-                        load_bias(ba, c_beg);
-                        sm100::tmem_wait_ld();
-                        for (int c0 = c_beg; c0 < c_end; c0 += 32) {
-                            const bool has_b = c0 + 16 < c_end;
-                            if (has_b) {
-                                sm100::tmem_ld16(t_row + c0 + 16, rb);
-                                load_bias(bb, c0 + 16);
-                            }
-                            requant(ra, ba, c0);
-                            sm100::tmem_wait_ld();
-                            if (!has_b)
-                                break;
-                            if (c0 + 32 < c_end) {
-                                sm100::tmem_ld16(t_row + c0 + 32, ra);
-                                load_bias(ba, c0 + 32);
-                            }
-                            requant(rb, bb, c0 + 16);
-                            sm100::tmem_wait_ld();
-                        }
+                        requant_pipelined(t_row, bias, ly.shift, out, row, c_beg, c_end);
                         sm100::tc_fence_before();
                         sm100::fence_proxy_async_smem();
                         tr(70 + l);
@@ -605,322 +662,6 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
         sm100::tmem_dealloc(tmem, p.tmem_cols);
 }
 
-// ------------------------------------------------------------------ duo schedule
-// Hidden-layer epilogue of one thread (= TMEM lane = tile row) over columns
-// [c_beg, c_end): (acc + bias) >> shift, saturated to u8, stored as the next
-// layer's K-major A operand at `out`.  The TMEM load of the next 16 columns is
-// in flight while the current 16 are requantised and stored.
-__device__ __forceinline__ void requant_columns(uint32_t t_row, const int32_t *bias, int sh, uint32_t out, int row,
-                                                int c_beg, int c_end) {
-    auto requant = [&](const int32_t(&r)[16], const int4(&b4)[4], int c0) {
-        uint32_t w[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            w[q] = sm100::pack_sat_u8x4((r[q * 4 + 0] + b4[q].x) >> sh, (r[q * 4 + 1] + b4[q].y) >> sh,
-                                        (r[q * 4 + 2] + b4[q].z) >> sh, (r[q * 4 + 3] + b4[q].w) >> sh);
-        sm100::st_shared_v4(out + (c0 >> 4) * 2048u + row * 16u, w[0], w[1], w[2], w[3]);
-    };
-    auto load_bias = [&](int4(&b4)[4], int c0) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
-    };
-    int32_t ra[16], rb[16];
-    int4 ba[4], bb[4];
-    sm100::tmem_ld16(t_row + c_beg, ra);
-    load_bias(ba, c_beg);
-    sm100::tmem_wait_ld();
-    for (int c0 = c_beg; c0 < c_end; c0 += 32) {
-        const bool has_b = c0 + 16 < c_end;
-        if (has_b) {
-            sm100::tmem_ld16(t_row + c0 + 16, rb);
-            load_bias(bb, c0 + 16);
-        }
-        requant(ra, ba, c0);
-        sm100::tmem_wait_ld();
-        if (!has_b)
-            break;
-        if (c0 + 32 < c_end) {
-            sm100::tmem_ld16(t_row + c0 + 32, ra);
-            load_bias(ba, c0 + 32);
-        }
-        requant(rb, bb, c0 + 16);
-        sm100::tmem_wait_ld();
-    }
-}
-
-// kDuo: resident weights with TWO jobs in flight.  The CTA's tiles alternate
-// between two slots; slot s owns activation buffer s (the one-hot, then every
-// hidden activation aliased over it: a layer's input is dead once its MMAs
-// completed), TMEM columns [s*cols/2, +cols/2) and an epilogue group of 8
-// warps (two per TMEM lane quadrant: half 0 drains columns [0, N/2) and reads
-// out, half 1 drains [N/2, N) and encodes the slot's next job).  The MMA warp
-// serves whichever slot's input is ready, so one slot's epilogue overlaps the
-// other slot's MMAs.  Barriers per slot: act_ready (256 epilogue threads: the
-// layer input is written / the accumulator was read) and d_full (commit).
-constexpr int kDuoThreads = 544;  // warp 0: weight load + MMA issue; warps 1-16: two epilogue groups
-
-template <int DOMAIN, int CM>
-__global__ void __launch_bounds__(kDuoThreads, 1) mlp_duo_kernel(const __grid_constant__ MlpParams p) {
-    using T = DomainTraits<DOMAIN>;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t *wbuf = smem + 2 * p.xbytes;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(wbuf + p.wbytes_pad);
-    uint64_t *w_ready = bars;        // weight image landed
-    uint64_t *act_ready = bars + 1;  // [2]
-    uint64_t *d_full = bars + 3;     // [2]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 5);
-
-    const int warp = threadIdx.x >> 5;
-    const long long ntiles = (p.n + kTileM - 1) / kTileM;
-    const long long nloc =
-        blockIdx.x < ntiles ? (ntiles - static_cast<long long>(blockIdx.x) + gridDim.x - 1) / gridDim.x : 0;
-    const uint32_t slot_cols = p.tmem_cols >> 1;
-
-    if (threadIdx.x == 0) {
-        sm100::mbar_init(w_ready, 1);
-        for (int s = 0; s < 2; ++s) {
-            sm100::mbar_init(&act_ready[s], 256);
-            sm100::mbar_init(&d_full[s], 1);
-        }
-        sm100::fence_barrier_init();
-    }
-    if (warp == 0)
-        sm100::tmem_alloc(tmem_slot, p.tmem_cols);
-    sm100::tc_fence_before();
-    __syncthreads();
-    sm100::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    Tracer tr;
-    if (p.trace && blockIdx.x == 0 && lane_id() == 0)
-        tr.buf = p.trace + static_cast<long long>(warp) * kTraceSlots;
-
-    if (warp == 0) {
-        // ------------------------------------------------ weight load + MMA issue
-        if (nloc > 0) {
-            if (lane_id() == 0) {
-                sm100::mbar_arrive_expect_tx(w_ready, static_cast<uint32_t>(p.wbytes));
-                for (int off = 0; off < p.wbytes; off += kStageBytes) {
-                    const int b = min(kStageBytes, p.wbytes - off);
-                    sm100::bulk_g2s(wbuf + off, p.wimg + off, static_cast<uint32_t>(b), w_ready);
-                }
-            }
-            __syncwarp();
-            sm100::mbar_wait(w_ready, 0);
-            const uint32_t sbase = sm100::smem_u32(smem), sW = sm100::smem_u32(wbuf);
-            long long k[2] = {0, 1};
-            int e[2] = {0, 0}, l[2] = {0, 0};
-            uint32_t aph[2] = {0u, 0u};
-            bool rem[2] = {nloc > 0, nloc > 1};
-            while (rem[0] || rem[1]) {
-                bool idle = true;
-#pragma unroll
-                for (int s = 0; s < 2; ++s) {
-                    if (!rem[s] || !__any_sync(kFull, sm100::mbar_test_wait(&act_ready[s], aph[s])))
-                        continue;
-                    idle = false;
-                    sm100::mbar_wait(&act_ready[s], aph[s]);  // acquire on every lane
-                    aph[s] ^= 1u;
-                    if (lane_id() == 0)
-                        tr(20 + l[s] + 4 * s);
-                    sm100::tc_fence_after();
-                    const MlpLayer ly = p.layer[e[s]][l[s]];
-                    const int nch = ly.K / kKChunk;
-                    const uint32_t cbytes = static_cast<uint32_t>(ly.N) * kKChunk;
-                    const uint32_t idesc = sm100::make_idesc_i8(ly.N);
-                    uint64_t adesc = sm100::make_smem_desc(sbase + s * p.xbytes, 2048u, 128u);
-                    uint64_t bdesc = sm100::make_smem_desc(sW + static_cast<uint32_t>(ly.woff), cbytes >> 1, 128u);
-                    const uint32_t dcol = tmem + s * slot_cols;
-                    if (sm100::elect_one()) {
-                        for (int j = 0; j < nch; ++j) {
-                            sm100::mma_i8(dcol, adesc, bdesc, idesc, j > 0 ? 1u : 0u);
-                            adesc += 4096u >> 4;
-                            bdesc += cbytes >> 4;
-                        }
-                        sm100::mma_commit(&d_full[s]);
-                    }
-                    __syncwarp();
-                    if (lane_id() == 0)
-                        tr(30 + l[s] + 4 * s);
-                    if (++l[s] == p.nl) {
-                        l[s] = 0;
-                        if (++e[s] == p.E) {
-                            e[s] = 0;
-                            k[s] += 2;
-                            rem[s] = k[s] < nloc;
-                        }
-                    }
-                }
-                if (idle)
-                    __nanosleep(32);  // leave the issue slots to this SM sub-partition's epilogue warps
-            }
-        }
-    } else {
-        // ------------------------------------------------ encode / epilogue / readout
-        const int ew = warp - 1;
-        const int g = ew >> 3;          // slot
-        const int half = (ew >> 2) & 1; // 0: drains [0, N/2) + reads out; 1: drains [N/2, N) + encodes
-        const int quad = warp & 3;      // TMEM lane quadrant this warp may access
-        const int row = quad * 32 + lane_id();
-        const uint32_t sX = sm100::smem_u32(smem) + g * p.xbytes;
-        const uint32_t t_row = tmem + g * slot_cols + (static_cast<uint32_t>(quad * 32) << 16);
-        uint64_t *my_ready = &act_ready[g];
-        uint64_t *my_full = &d_full[g];
-        uint32_t dph = 0;
-
-        auto load_state = [&](long long kk, uint64_t &lo_, uint64_t &hi_) {
-            lo_ = hi_ = 0;
-            const long long s_ = (blockIdx.x + kk * gridDim.x) * kTileM + row;
-            if (kk < nloc && s_ < p.n) {
-                if constexpr (T::PB == 16) {
-                    const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2 *>(p.packed) + s_);
-                    lo_ = v.x;
-                    hi_ = v.y;
-                } else {
-                    lo_ = __ldcs(reinterpret_cast<const unsigned long long *>(p.packed) + s_);
-                }
-            }
-        };
-        auto state_bad = [&](uint64_t lo_, uint64_t hi_) {
-            bool b = false;
-#pragma unroll
-            for (int q = 0; q < T::NNZ; ++q) {
-                const int j = position_feature<DOMAIN>(lo_, hi_, q);
-                b |= j < 0 || j >= T::F;
-            }
-            return b;
-        };
-        auto tile_valid = [&](long long kk) { return kk < nloc && (blockIdx.x + kk * gridDim.x) * kTileM + row < p.n; };
-        const int nchunk = p.Fpad / 16;
-        auto encode = [&](uint64_t lo_, uint64_t hi_, bool live_) {
-            tr(40);
-            for (int c16 = 0; c16 < nchunk; ++c16)
-                sm100::st_shared_v4(sX + c16 * 2048u + row * 16u, 0u, 0u, 0u, 0u);
-            if (live_) {
-#pragma unroll
-                for (int q = 0; q < T::NNZ; ++q) {
-                    const int j = position_feature<DOMAIN>(lo_, hi_, q);
-                    sm100::st_shared_u8(sX + (j >> 4) * 2048u + row * 16u + (j & 15), 1u);
-                }
-            }
-            sm100::fence_proxy_async_smem();
-            tr(41);
-            sm100::mbar_arrive(my_ready);
-        };
-
-        uint64_t nlo = 0, nhi = 0;
-        load_state(g, nlo, nhi);
-        if (g < nloc) {  // the slot's first job: half 1 encodes, half 0 has nothing to drain
-            if (half)
-                encode(nlo, nhi, tile_valid(g) && !state_bad(nlo, nhi));
-            else
-                sm100::mbar_arrive(my_ready);
-        }
-        for (long long k = g; k < nloc; k += 2) {
-            const long long st = (blockIdx.x + k * gridDim.x) * kTileM + row;
-            const bool valid = st < p.n;
-            const uint64_t lo = nlo, hi = nhi;
-            load_state(k + 2, nlo, nhi);
-            const bool bad = valid && state_bad(lo, hi);
-            const bool reader = half == 0;
-            const int hpdb = (p.pdb.entries && reader && valid) ? pdb_fetch<DOMAIN>(p.pdb, lo) : 0;
-            if (bad && reader)
-                raise_error(p.err, kErrState);
-            const bool live = valid && !bad;
-            int hmin = 0x7fffffff;
-            bool dist_bad = false;
-            for (int e = 0; e < p.E; ++e) {
-                for (int l = 0; l < p.nl; ++l) {
-                    const MlpLayer &ly = p.layer[e][l];
-                    tr(50 + l);
-                    sm100::mbar_wait(my_full, dph);
-                    dph ^= 1u;
-                    tr(60 + l);
-                    sm100::tc_fence_after();
-                    const int32_t *bias = p.bias + ly.boff;
-                    if (l + 1 < p.nl) {
-                        const int hN = ly.N >> 1;
-                        requant_columns(t_row, bias, ly.shift, sX, row, half * hN, half * hN + hN);
-                        sm100::tc_fence_before();
-                        sm100::fence_proxy_async_smem();
-                        tr(70 + l);
-                        sm100::mbar_arrive(my_ready);
-                        continue;
-                    }
-                    const bool next_member = e + 1 < p.E;
-                    const bool has_next = next_member || k + 2 < nloc;
-                    if (!reader) {
-                        // the slot's next job: X is free (this job's last MMAs completed)
-                        if (has_next) {
-                            if (next_member)
-                                encode(lo, hi, live);
-                            else
-                                encode(nlo, nhi, tile_valid(k + 2) && !state_bad(nlo, nhi));
-                        }
-                        continue;
-                    }
-                    // output layer: exact integer logits -> certified readout
-                    int32_t v[CM];
-#pragma unroll
-                    for (int c0 = 0; c0 < CM; c0 += 16) {
-                        if (c0 < p.C) {
-                            int32_t r[16];
-                            sm100::tmem_ld16(t_row + c0, r);
-                            int4 b4[4];
-#pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
-                            sm100::tmem_wait_ld();
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                v[c0 + 4 * q + 0] = r[4 * q + 0] + b4[q].x;
-                                v[c0 + 4 * q + 1] = r[4 * q + 1] + b4[q].y;
-                                v[c0 + 4 * q + 2] = r[4 * q + 2] + b4[q].z;
-                                v[c0 + 4 * q + 3] = r[4 * q + 3] + b4[q].w;
-                            }
-                        }
-                    }
-                    sm100::tc_fence_before();
-                    if (has_next)
-                        sm100::mbar_arrive(my_ready);  // accumulator read: the next job's L0 may start
-                    tr(81);
-                    if (p.logits_out && valid) {
-                        double *dst = p.logits_out + (static_cast<size_t>(st) * p.E + e) * p.C;
-                        for (int c = 0; c < p.C; ++c)
-                            dst[c] = static_cast<double>(v[c]) * p.scale_d[e];
-                    }
-                    bool fb = false;
-                    const int h = readout_certified<CM>(v, p.C, p.scale_f[e], p.scale_d[e], p.rk, &dist_bad, &fb);
-                    hmin = min(hmin, h);
-                    tr(fb ? 83 : 82);
-                    tr(80);
-                }
-            }
-            if (reader && valid) {
-                if (dist_bad)
-                    raise_error(p.err, kErrDistribution);
-                int h = (live && !dist_bad) ? hmin : 0;
-                if (p.pdb.entries && live) {
-                    if (hpdb < 0) {
-                        raise_error(p.err, kErrState);
-                        h = 0;
-                    } else {
-                        h = pdb_combine(p.pdb, h, hpdb);
-                    }
-                }
-                p.h_out[st] = h;
-            }
-        }
-    }
-
-    __syncwarp();
-    sm100::tc_fence_before();
-    __syncthreads();
-    sm100::tc_fence_after();
-    if (warp == 0)
-        sm100::tmem_dealloc(tmem, p.tmem_cols);
-}
-
 // ------------------------------------------------------------------ wide schedule
 // kWide: hidden layers of any width up to kMaxHidden.  A tile's activations
 // no longer fit in shared memory (128 x 1632 B = 204 KB for the paper's
@@ -949,47 +690,6 @@ __device__ __forceinline__ int wide_ks(int l, int cw, int ns, int nk, int stage_
     return max(1, min(nk, stage_bytes / kb));
 }
 
-// Hidden-layer epilogue into global scratch: TMEM columns [t0, t0 + n) hold
-// output columns [o0, o0 + n) of this thread's row.
-__device__ __forceinline__ void requant_to_global(uint32_t t_row, int t0, const int32_t *bias, int o0, int n, int sh,
-                                                  uint8_t *out, int row) {
-    auto store = [&](const int32_t(&r)[16], const int4(&b4)[4], int oc) {
-        uint32_t w[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            w[q] = sm100::pack_sat_u8x4((r[q * 4 + 0] + b4[q].x) >> sh, (r[q * 4 + 1] + b4[q].y) >> sh,
-                                        (r[q * 4 + 2] + b4[q].z) >> sh, (r[q * 4 + 3] + b4[q].w) >> sh);
-        sm100::st_global_v4(out + (oc >> 5) * 4096 + ((oc >> 4) & 1) * 2048 + row * 16, w[0], w[1], w[2], w[3]);
-    };
-    auto load_bias = [&](int4(&b4)[4], int oc) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + oc) + q);
-    };
-    int32_t ra[16], rb[16];
-    int4 ba[4], bb[4];
-    sm100::tmem_ld16(t_row + t0, ra);
-    load_bias(ba, o0);
-    sm100::tmem_wait_ld();
-    for (int j = 0; j < n; j += 32) {
-        const bool has_b = j + 16 < n;
-        if (has_b) {
-            sm100::tmem_ld16(t_row + t0 + j + 16, rb);
-            load_bias(bb, o0 + j + 16);
-        }
-        store(ra, ba, o0 + j);
-        sm100::tmem_wait_ld();
-        if (!has_b)
-            break;
-        if (j + 32 < n) {
-            sm100::tmem_ld16(t_row + t0 + j + 32, ra);
-            load_bias(ba, o0 + j + 32);
-        }
-        store(rb, bb, o0 + j + 16);
-        sm100::tmem_wait_ld();
-    }
-}
-
 template <int DOMAIN, int CM, bool PAIR>
 __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_constant__ MlpParams p) {
     using T = DomainTraits<DOMAIN>;
@@ -997,7 +697,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
     extern __shared__ __align__(1024) uint8_t smem[];
     const int stage_bytes = p.stage_bytes;
     uint8_t *stages = smem + p.xbytes;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(stages + p.stages * stage_bytes);
+    uint8_t *bias_sm = stages + p.stages * stage_bytes;  // [bias_bytes] optional
+    uint64_t *bars = reinterpret_cast<uint64_t *>(bias_sm + p.bias_bytes);
     uint64_t *full = bars;                          // [kWideMaxStages] local TMA landed
     uint64_t *empty = bars + kWideMaxStages;        // [kWideMaxStages] pair's MMAs done with the stage
     uint64_t *full2 = bars + 2 * kWideMaxStages;    // [kWideMaxStages] PAIR, even CTA: peer's stage landed
@@ -1007,7 +708,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
     uint64_t *act_done = tmem_free + 2;             // hidden layer written to scratch (256)
     uint64_t *x_ready2 = act_done + 1;              // PAIR, even CTA: peer's one-hot written
     uint64_t *tmem_free2 = x_ready2 + 1;            // [2] PAIR, even CTA: peer's buffer drained
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_free2 + 2);
+    uint64_t *b_ready = tmem_free2 + 2;             // bias staged
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(b_ready + 1);
     uint32_t *sink = tmem_slot + 1;                 // PAIR, even CTA: target of the peer's st.async signals
 
     const int warp = threadIdx.x >> 5;
@@ -1035,6 +737,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
         }
         sm100::mbar_init(act_done, 256);
         sm100::mbar_init(x_ready2, 1);
+        sm100::mbar_init(b_ready, 1);
         sm100::fence_barrier_init();
     }
     if (warp == 1) {
@@ -1050,12 +753,16 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     Tracer tr;
-    if (p.trace && blockIdx.x == 0 && lane_id() == 0)
+    if (Tracer::kOn && p.trace && blockIdx.x == 0 && lane_id() == 0)
         tr.buf = p.trace + static_cast<long long>(warp) * kTraceSlots;
 
     if (warp == 0) {
         // ------------------------------------------------ producer: [A ks x 4 KB][B ks x chunk part] stages
         if (lane_id() == 0 && nloc > 0) {
+            if (p.bias_bytes) {
+                sm100::mbar_arrive_expect_tx(b_ready, static_cast<uint32_t>(p.bias_bytes));
+                sm100::bulk_g2s(bias_sm, p.bias, static_cast<uint32_t>(p.bias_bytes), b_ready);
+            }
             int s = 0;
             uint32_t ph = 0, adph = 0;
             for (long long k = 0; k < nloc; ++k)
@@ -1169,11 +876,11 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
                             long long wsum = 0;  // debug timeline: cycles spent waiting for stages
                             for (int kc = 0; kc < nk; kc += ks) {
                                 const int kn = min(ks, nk - kc);
-                                const long long tw0 = tr.buf ? clock64() : 0;
+                                const long long tw0 = tr.on() ? clock64() : 0;
                                 sm100::mbar_wait(&full[s], ph);
                                 if constexpr (PAIR)
                                     sm100::mbar_wait(&full2[s], ph);
-                                if (tr.buf)
+                                if (tr.on())
                                     wsum += clock64() - tw0;
                                 sm100::tc_fence_after();
                                 uint64_t ad = l == 0 ? xd : a0 + soff, bd = b0 + soff;
@@ -1210,8 +917,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
                             __syncwarp();
                             if (lane_id() == 0) {
                                 tr(30 + l);
-                                if (tr.buf && tr.n < kTraceSlots)
-                                    tr.buf[tr.n++] = (wsum << 8) | 90;  // value, not a timestamp
+                                tr.value(wsum, 90);
                             }
                         }
                     }
@@ -1240,20 +946,13 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
                 }
             }
         };
-        auto state_bad = [&](uint64_t lo_, uint64_t hi_) {
-            bool bd = false;
-#pragma unroll
-            for (int q = 0; q < T::NNZ; ++q) {
-                const int j = position_feature<DOMAIN>(lo_, hi_, q);
-                bd |= j < 0 || j >= T::F;
-            }
-            return bd;
-        };
+        auto state_bad = [&](uint64_t lo_, uint64_t hi_) { return state_out_of_range<DOMAIN>(lo_, hi_); };
         auto tile_valid = [&](long long kk) { return kk < nloc && state_of(kk) < p.n; };
-        const int nchunk16 = p.Fpad / 16;
+        constexpr int kX16 = (T::F + 31) / 32 * 2;  // 16-column chunks of the one-hot tile (Fpad / 16)
         auto encode = [&](uint64_t lo_, uint64_t hi_, bool live_) {
             tr(40);
-            for (int c16 = 0; c16 < nchunk16; ++c16)
+#pragma unroll
+            for (int c16 = 0; c16 < kX16; ++c16)
                 sm100::st_shared_v4(sX + c16 * 2048u + row * 16u, 0u, 0u, 0u, 0u);
             if (live_) {
 #pragma unroll
@@ -1271,6 +970,9 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
         load_state(0, nlo, nhi);
         if (encoder && nloc > 0)
             encode(nlo, nhi, tile_valid(0) && !state_bad(nlo, nhi));
+        const uint32_t bias_s = p.bias_bytes ? sm100::smem_u32(bias_sm) : 0u;
+        if (p.bias_bytes && nloc > 0)
+            sm100::mbar_wait(b_ready, 0);
         for (long long k = 0; k < nloc; ++k) {
             const long long st = state_of(k);
             const bool valid = st < p.n;
@@ -1299,7 +1001,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
                         sm100::tc_fence_after();
                         if (hidden) {
                             const int half = cw >> 1;  // multiple of 16: widths are padded to 32
-                            requant_to_global(t_row, grp * half, bias, c0 + grp * half, half, ly.shift, out, row);
+                            requant_block<true>(t_row, grp * half, bias, c0 + grp * half, half, ly.shift, 0u, out, row,
+                                                bias_s ? bias_s + ly.boff * 4u : 0u);
                             sm100::tc_fence_before();
                             sm100::mbar_arrive(&tmem_free[b]);
                             tr(70 + l);
@@ -1399,13 +1102,7 @@ template <int DOMAIN, int CM>
 int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
     auto kern = p.mode != kWide ? mlp_fused_kernel<DOMAIN, CM>
                 : (p.cluster == 2 ? mlp_wide_kernel<DOMAIN, CM, true> : mlp_wide_kernel<DOMAIN, CM, false>);
-    int threads = kMlpThreads;
-    if constexpr (CM == 32) {  // the duo schedule is built for C <= 32 (register budget at 544 threads)
-        if (p.mode == kDuo) {
-            kern = mlp_duo_kernel<DOMAIN, CM>;
-            threads = kDuoThreads;
-        }
-    }
+    const int threads = kMlpThreads;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(m->smem));
     if (e != cudaSuccess) {
@@ -1597,22 +1294,19 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
             c <<= 1;
         return c;
     };
-    // 0) a layer wider than 512 (or nothing else fits): wide (activations in
-    //    L2-resident global scratch, A and B streamed)
+    // 0) a layer wider than 256 (or nothing else fits): wide (activations in
+    //    L2-resident global scratch, A and B streamed; h512 1.27 vs 1.17 G/s split)
     // 1) every layer <= 256 wide and the whole weight image fits next to one
     //    activation set: resident
     // 2) every layer <= 256 wide and two activation sets fit: pair (streamed)
-    // 3) every layer <= 512 wide: split (streamed)
-    // BIDA_MLP_FORCE_MODE=wide|duo|resident|pair|split (tests): use that schedule
-    // when it fits.  duo (two resident-weight jobs in flight, C <= 32) is
-    // opt-in only: measured slower than resident (profiles/r1_notes.md).
+    // 3) every layer <= 512 wide: split (streamed; BIDA_MLP_FORCE_MODE=split)
+    // BIDA_MLP_FORCE_MODE=wide|resident|pair|split (tests): use that schedule
+    // when it fits.
     const char *force = std::getenv("BIDA_MLP_FORCE_MODE");
     const std::string fm = force ? force : "";
     int Kmax = Fpad;
     for (uint32_t l = 0; l < L; ++l)
         Kmax = std::max(Kmax, Hp[l]);
-    const size_t xduo = static_cast<size_t>(kTileM) * Kmax;  // one aliased activation buffer per slot
-    const bool fit_duo = Nmax <= 256 && C <= 32 && 2 * xduo + p.wbytes_pad + bar_bytes <= budget;
     const bool fit_res = Nmax <= 256 && set1 + p.wbytes_pad + bar_bytes <= budget;
     const bool fit_pair = Nmax <= 256 && stages_for(2 * set1) >= 2;
     const bool want_split = fm == "split" && stages_for(set1) >= 2;
@@ -1623,13 +1317,15 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     const bool wide_pair = wpv && wpv[0] == '1';
     // a stage holds 3 K steps of a full chunk: [A 3 x 4 KB][B 3 x 256 x 32 B (/2 per CTA of a pair)]
     const int wide_stage = 3 * (kWideStageA + kWideChunk * kKChunk / (wide_pair ? 2 : 1));
-    const size_t wide_bars = 8 * (3 * kWideMaxStages + 9) + 16;
+    const size_t wide_bars = 8 * (3 * kWideMaxStages + 10) + 16;
     const size_t xwide = static_cast<size_t>(kTileM) * Fpad;
+    const size_t wide_bias = bias.size() * 4;  // staged in shared memory when 4 stages still fit
+    const size_t wide_bias_sm = xwide + wide_bars + wide_bias + 4 * static_cast<size_t>(wide_stage) <= budget ? wide_bias : 0;
     const int wide_stages =
-        xwide + wide_bars + 2 * wide_stage > budget
+        xwide + wide_bars + wide_bias_sm + 2 * wide_stage > budget
             ? 0
-            : static_cast<int>(std::min<size_t>(kWideMaxStages, (budget - xwide - wide_bars) / wide_stage));
-    if (wide_stages >= 2 && (fm == "wide" || Nmax > 512 || (!fit_res && !fit_pair && !fit_split))) {
+            : static_cast<int>(std::min<size_t>(kWideMaxStages, (budget - xwide - wide_bars - wide_bias_sm) / wide_stage));
+    if (wide_stages >= 2 && (fm == "wide" || (Nmax > 256 && fm != "split") || (!fit_res && !fit_pair && !fit_split))) {
         p.mode = kWide;
         p.stages = wide_stages;
         p.xbytes = static_cast<int>(xwide);
@@ -1637,16 +1333,10 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
         p.tmem_cols = 512u;
         p.sbytes = static_cast<long long>(kTileM) * Kmax;
         p.stage_bytes = wide_stage;
+        p.bias_bytes = static_cast<int>(wide_bias_sm);
         p.cluster = wide_pair ? 2 : 1;
-        m->smem = xwide + static_cast<size_t>(wide_stages) * wide_stage + wide_bars;
-    } else if (fit_duo && fm == "duo") {  // two jobs in flight, resident weights (opt-in: see r1_notes.md)
-        p.mode = kDuo;
-        p.stages = 0;
-        p.xbytes = static_cast<int>(xduo);
-        p.ybytes = 0;
-        p.tmem_cols = 2 * pow2cols(Nmax);
-        m->smem = 2 * xduo + p.wbytes_pad + bar_bytes;
-    } else if (!want_split && fit_res && (fm.empty() || fm == "resident" || fm == "duo" || (fm == "pair" && !fit_pair))) {  // (TMEM double-buffered by job)
+        m->smem = xwide + static_cast<size_t>(wide_stages) * wide_stage + wide_bias_sm + wide_bars;
+    } else if (!want_split && fit_res && (fm.empty() || fm == "resident" || (fm == "pair" && !fit_pair))) {  // (TMEM double-buffered by job)
         p.mode = kResident;
         p.stages = 0;
         p.tmem_cols = 512u;

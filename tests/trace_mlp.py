@@ -9,6 +9,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["BIDA_GPU_TRACE"] = "1"  # the diagnostic library (built in the build container: build(trace=True))
 import paper_2507_11916_b200 as bida  # noqa: E402
 from paper_2507_11916_b200 import _native  # noqa: E402
 from paper_2507_11916_b200.models import make_bmlp1  # noqa: E402
