@@ -156,7 +156,9 @@ def test_bad_models_rejected():
 def test_every_schedule_matches_oracle(orc, monkeypatch, schedule, hidden, C, E):
     """The kernel schedules (wide / resident weights / tile ping-pong / N-half
     pipelined split) give identical, oracle-exact results, including odd
-    K-chunk splits (96, 160) and layers wider than the previous one."""
+    K-chunk splits (96, 160) and layers wider than the previous one.  Three
+    CTAs: several tiles each, so both slots of the two-tile schedules run."""
+    monkeypatch.setenv("BIDA_MLP_MAX_CTAS", "3")
     monkeypatch.setenv("BIDA_MLP_FORCE_MODE", schedule)
     blob = make_bmlp1("rc", hidden=hidden, classes=C, ensemble=E, seed=len(hidden) * 100 + C)
     packed = bida.random_walks("rc", 777, 0, 30, seed=C + E)
