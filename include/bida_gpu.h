@@ -91,7 +91,10 @@ int bida_gpu_linear_load(int device, int domain, const char *path, double quanti
                          bida_gpu_evaluator **out);
 
 /* BMLP1 integer MLP ensemble (project format; the reference has
- * no MLP).  Same readout as the linear model. */
+ * no MLP).  Same readout as the linear model.  Hidden widths 1..4096 (the
+ * kernel schedule -- weights resident in shared memory, streamed, or wide
+ * with activations in L2-resident scratch -- is chosen at load time), up to 4
+ * hidden layers, C <= 256 classes, E <= 8 members. */
 int bida_gpu_mlp_create_bmlp1(int device, int domain, const void *blob, size_t len,
                               double quantile, bida_gpu_evaluator **out);
 int bida_gpu_mlp_load(int device, int domain, const char *path, double quantile,
