@@ -1,0 +1,38 @@
+"""SURVEY §8(f) row 1 measurement on one B200: Batch IDA* nodes/s with the
+reference's Evaluator (tools/bin/bida_search) vs the ring evaluator
+(tools/bin/bida_search_ring), both with GpuBackend (network + PDB on the
+device), swept over evaluators per GPU and agents per evaluator.  Rubik's
+walk-15, Table-1 mode, BMLP1 480-128-128-21.  Not a pytest test; -> profiles/."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2507_11916_b200.models import make_bmlp1  # noqa: E402
+
+secs = sys.argv[1] if len(sys.argv) > 1 else "8"
+model = "/tmp/ring128.bmlp"
+open(model, "wb").write(make_bmlp1("rc", hidden=[128, 128], classes=21, seed=2507))
+ncpu = len(os.sched_getaffinity(0))
+common = ["--domain", "rc", "--walks", "1:15:15:2508", "--model", "mlp:" + model, "--table1-pdb", "5",
+          "--time-limit", secs, "--mode", "gpu", "--gpu-pdb", "--work-num", "128", "--threads", str(ncpu)]
+runs = []
+for E in (1, 2, 8):
+    for B, t in ((16384, 25), (4096, 0)):
+        runs.append(("reference", "bida_search", E, 1, B, t))
+        for K in (2, 4):
+            runs.append(("ring", "bida_search_ring", E, K, B, t))
+for impl, exe, E, K, B, t in runs:
+    out = subprocess.run([os.path.join(ROOT, "tools", "bin", exe), *common, "--evaluators", str(E), "--batch", str(B),
+                          "--timeout-us", str(t)], capture_output=True, text=True, timeout=600,
+                         env={**os.environ, "BIDA_EVAL_AGENTS": str(K)})
+    rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    if out.returncode or not rows:
+        print(json.dumps({"impl": impl, "evaluators": E, "agents": K, "error": out.stderr[-300:]}), flush=True)
+        continue
+    r = rows[0]
+    r.pop("iterations", None)
+    r.update(impl=impl, agents=K, host_threads=ncpu)
+    print(json.dumps(r), flush=True)

@@ -143,3 +143,50 @@ def test_batch_astar_with_gpu_evaluator(tmp_path, manhattan_blins):
     for i, m in by.items():
         assert m["gpu"]["status"] == m["cpu"]["status"] == "solved"
         assert m["gpu"]["cost"] == m["cpu"]["cost"]
+
+
+RING = os.path.join(ROOT, "tools", "bin", "bida_search_ring")
+
+
+def test_ring_evaluator_gpu_matches_cpu(tmp_path, manhattan_blins):
+    """SURVEY §8(f) row 1 on the device: the ring evaluator (lock-free submit
+    ring, K concurrent agents per evaluator) with GpuBackend vs the same
+    driver with the reference's CPU LinearModelBackend — identical trees on
+    the stp8 grid, 2 agents so two device batches are in flight."""
+    if not os.path.exists(RING):
+        pytest.fail(f"{RING} not built")
+    g = np.load(os.path.join(GOLDEN, "instances.npz"))
+    inst = write_instances(tmp_path, "stp8.txt", g["stp8_100"], "stp3")
+    for n, k, B, t in [(2, 4, 32, 200), (4, 4, 256, -1), (8, 8, 64, 0)]:
+        out = subprocess.run([RING, "--domain", "stp3", "--instances", inst, "--model", "linear:" + manhattan_blins[0],
+                              "--mode", "both", "--threads", str(n), "--work-num", str(k), "--batch", str(B),
+                              "--timeout-us", str(t), "--count", "40"],
+                             capture_output=True, text=True, timeout=900, env={**os.environ, "BIDA_EVAL_AGENTS": "2"})
+        assert out.returncode == 0, out.stderr
+        rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+        assert all(r["evaluator_impl"] == "ring" for r in rows)
+        compare(rows)
+
+
+def test_ring_evaluator_rc_table1_gpu_pdb(tmp_path):
+    """Table-1 mode through the ring evaluator: network + PDB on the device,
+    costs and threshold histories equal to the reference-evaluator CPU run."""
+    from paper_2507_11916_b200.models import make_bmlp1
+
+    if not os.path.exists(RING):
+        pytest.fail(f"{RING} not built")
+    blob = make_bmlp1("rc", hidden=[128, 128], classes=21, ensemble=1, seed=11)
+    path = tmp_path / "m.bmlp"
+    path.write_bytes(blob)
+    common = ["--domain", "rc", "--walks", "4:6:8:5", "--model", "mlp:" + str(path), "--table1-pdb", "4",
+              "--threads", "4", "--work-num", "4", "--batch", "1024", "--timeout-us", "200", "--time-limit", "300"]
+    cpu = run([*common, "--mode", "cpu"])
+    out = subprocess.run([RING, *common, "--mode", "gpu", "--gpu-pdb", "--evaluators", "2"],
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr
+    gpu = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(gpu) == len(cpu) == 4
+    for c, g_ in zip(cpu, gpu):
+        assert g_["status"] == c["status"] == "solved"
+        assert g_["cost"] == c["cost"] and g_["thresholds"] == c["thresholds"]
+        assert [it[:3] for it in g_["iterations"][:-1]] == [it[:3] for it in c["iterations"][:-1]]

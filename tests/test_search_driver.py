@@ -66,3 +66,53 @@ def test_gpu_mode_without_device_fails_cleanly(man3):
         pytest.skip("a GPU is present")
     rc, rows, err = run(["--domain", "stp3", "--walks", "1:5:5:1", "--model", "linear:" + man3, "--mode", "gpu"])
     assert rc != 0 and "GpuBackend" in err
+
+
+RING = os.path.join(ROOT, "tools", "bin", "bida_search_ring")
+
+
+@pytest.mark.skipif(not os.path.exists(RING), reason="tools/bin/bida_search_ring not built")
+@pytest.mark.parametrize("timeout_us", ["200", "0", "-1"])
+def test_ring_evaluator_matches_reference_evaluator(tmp_path, man3, timeout_us):
+    """the same batch_idastar with the reference's Evaluator
+    (batch_eval.hpp:193-381) and with the ring evaluator (include/
+    bida_ring_evaluator.hpp) over the reference's CPU LinearModelBackend:
+    identical costs, threshold histories and non-final per-iteration counts,
+    under each flush policy (timeout > 0, == 0, < 0 = full or forced only)."""
+    g = np.load(os.path.join(ROOT, "tests", "golden", "instances.npz"))
+    inst = tmp_path / "stp8.txt"
+    inst.write_text("\n".join("stp 3 " + " ".join(str((int(v) >> (4 * c)) & 15) for c in range(9))
+                              for v in g["stp8_100"][:40]) + "\n")
+    args = ["--domain", "stp3", "--instances", str(inst), "--model", "linear:" + man3, "--mode", "cpu",
+            "--threads", "4", "--work-num", "4", "--batch", "32", "--timeout-us", timeout_us]
+    rc, ref, err = run(args)
+    assert rc == 0, err
+    out = subprocess.run([RING, *args], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    ring = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(ref) == len(ring) == 40
+    for a, b in zip(ref, ring):
+        assert a["evaluator_impl"] == "reference" and b["evaluator_impl"] == "ring"
+        assert a["status"] == b["status"] == "solved"
+        assert a["cost"] == b["cost"] and a["thresholds"] == b["thresholds"]
+        assert [it[:3] for it in a["iterations"][:-1]] == [it[:3] for it in b["iterations"][:-1]]
+        assert b["assertion_violations"] == 0 and b["batch_items"] > 0
+
+
+@pytest.mark.skipif(not os.path.exists(RING), reason="tools/bin/bida_search_ring not built")
+def test_ring_evaluator_rc_tablesim_multi_evaluator():
+    """Rubik's walks through the ring evaluator with 2 evaluators x 2 agents and
+    the corner-PDB Table-1 backend: every instance solved at the same cost as
+    the reference evaluator."""
+    args = ["--domain", "rc", "--walks", "3:5:7:9", "--model", "mlp:/dev/null", "--mode", "pdb",
+            "--table1-pdb", "4", "--threads", "4", "--work-num", "8", "--batch", "64", "--timeout-us", "0",
+            "--evaluators", "2"]
+    rc, ref, err = run(args)
+    assert rc == 0, err
+    out = subprocess.run([RING, *args], capture_output=True, text=True, timeout=300,
+                         env={**os.environ, "BIDA_EVAL_AGENTS": "2"})
+    assert out.returncode == 0, out.stderr
+    ring = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert [r["status"] for r in ring] == ["solved"] * 3
+    assert [r["cost"] for r in ring] == [r["cost"] for r in ref]
+    assert [r["thresholds"] for r in ring] == [r["thresholds"] for r in ref]

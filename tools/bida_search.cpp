@@ -197,6 +197,12 @@ std::vector<Instance<D>> get_instances(const Args &a) {
     return v;
 }
 
+#ifdef BIDA_RING_EVALUATOR
+constexpr const char *kEvaluatorImpl = "ring"; // include/bida_ring_evaluator.hpp
+#else
+constexpr const char *kEvaluatorImpl = "reference"; // batch_eval.hpp:193-473
+#endif
+
 const char *status_name(SearchStatus s) {
     switch (s) {
     case SearchStatus::Solved: return "solved";
@@ -249,6 +255,7 @@ int run(const Args &a) {
             }
             js << "], \"threads\": " << a.threads << ", \"work_num\": " << a.work_num << ", \"batch\": " << a.batch
                << ", \"timeout_us\": " << a.timeout_us << ", \"evaluators\": " << a.evaluators
+               << ", \"evaluator_impl\": \"" << kEvaluatorImpl << "\""
                << ", \"immediate\": " << (a.immediate ? "true" : "false")
                << ", \"table1_corners\": " << a.table1_corners << ", \"gpu_pdb\": " << (a.gpu_pdb ? "true" : "false")
                << ", \"algo\": \"" << a.algo << "\"}";
