@@ -61,6 +61,7 @@ int packed_bytes(int domain) {
 // states in flight on kSlots streams, so the H2D copy of chunk i+1.. overlaps
 // the kernel of chunk i and the D2H of chunk i-1 (copy engines are full duplex).
 constexpr int kSlots = 4;
+constexpr int kZcLanes = 4;
 
 struct bida_gpu_evaluator {
     int kind = 0, domain = 0, F = 0, C = 0, E = 0, device = 0;
@@ -91,9 +92,18 @@ struct bida_gpu_evaluator {
     int32_t *d_h[kSlots] = {};
     int *err_host = nullptr; // mapped pinned, kErrWords ints
     int *err_dev = nullptr;
-    // small-batch zero-copy path: mapped pinned in/out read/written by the kernel
-    void *zc_in = nullptr, *zc_in_dev = nullptr;
-    int32_t *zc_out = nullptr, *zc_out_dev = nullptr;
+    // small-batch zero-copy path: mapped pinned in/out read/written by the
+    // kernel, kZcLanes independent lanes (own lock, stream and buffers) so
+    // concurrent callers on one handle (the ring evaluator's agents,
+    // include/bida_ring_evaluator.hpp) keep several batches on the device
+    struct ZcLane {
+        std::mutex mu;
+        cudaStream_t st = nullptr;
+        void *in = nullptr, *in_dev = nullptr;
+        int32_t *out = nullptr, *out_dev = nullptr;
+    } zc[kZcLanes];
+    std::atomic<unsigned> zc_next{0};
+    std::mutex err_mu;
     std::atomic<int64_t> zc_calls{0};
     // PDB correction (bida_gpu_attach_pdb)
     uint8_t *d_pdb = nullptr;
@@ -172,6 +182,10 @@ int launch(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h
 }
 
 int collect_errors(bida_gpu_evaluator *ev) {
+    // one error word set per handle: with concurrent calls an error is
+    // reported by whichever call collects it first (errors mean corrupt
+    // states or non-finite logits, never a normal search)
+    std::lock_guard<std::mutex> lk(ev->err_mu);
     volatile int *e = ev->err_host;
     int rc = BIDA_OK;
     if (e[kErrState])
@@ -228,10 +242,13 @@ int common_init(bida_gpu_evaluator *ev, int device) {
                            cudaHostAllocMapped));
     std::memset(ev->err_host, 0, kErrWords * sizeof(int));
     CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&ev->err_dev), ev->err_host, 0));
-    CUDA_TRY(cudaHostAlloc(&ev->zc_in, kZeroCopyMax * 16, cudaHostAllocMapped | cudaHostAllocWriteCombined));
-    CUDA_TRY(cudaHostGetDevicePointer(&ev->zc_in_dev, ev->zc_in, 0));
-    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&ev->zc_out), kZeroCopyMax * 4, cudaHostAllocMapped));
-    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&ev->zc_out_dev), ev->zc_out, 0));
+    for (auto &ln : ev->zc) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking));
+        CUDA_TRY(cudaHostAlloc(&ln.in, kZeroCopyMax * 16, cudaHostAllocMapped | cudaHostAllocWriteCombined));
+        CUDA_TRY(cudaHostGetDevicePointer(&ln.in_dev, ln.in, 0));
+        CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&ln.out), kZeroCopyMax * 4, cudaHostAllocMapped));
+        CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&ln.out_dev), ln.out, 0));
+    }
     return BIDA_OK;
 }
 
@@ -249,8 +266,12 @@ void release(bida_gpu_evaluator *ev) {
         if (ev->stream[s]) cudaStreamDestroy(ev->stream[s]);
     }
     if (ev->err_host) cudaFreeHost(ev->err_host);
-    if (ev->zc_in) cudaFreeHost(ev->zc_in);
-    if (ev->zc_out) cudaFreeHost(ev->zc_out);
+    for (auto &ln : ev->zc) {
+        if (ln.st) cudaStreamSynchronize(ln.st);
+        if (ln.in) cudaFreeHost(ln.in);
+        if (ln.out) cudaFreeHost(ln.out);
+        if (ln.st) cudaStreamDestroy(ln.st);
+    }
     if (ev->d_Wt) cudaFree(ev->d_Wt);
     if (ev->d_rowflag) cudaFree(ev->d_rowflag);
     if (ev->d_pdb) cudaFree(ev->d_pdb);
@@ -492,14 +513,29 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         return fail(BIDA_ERR_INVALID_ARGUMENT, "bad batch arguments");
     if (n == 0)
         return BIDA_OK;
-    std::lock_guard<std::mutex> lk(ev->mu);
     CUDA_TRY(cudaSetDevice(ev->device));
     if (n <= kZeroCopyMax && !logits_out) {
+        // first free lane from a rotating start; block on one if all are busy
+        const unsigned start = ev->zc_next.fetch_add(1, std::memory_order_relaxed);
+        std::unique_lock<std::mutex> llk;
+        bida_gpu_evaluator::ZcLane *ln = nullptr;
+        for (int k = 0; k < kZcLanes && !ln; ++k) {
+            auto &cand = ev->zc[(start + k) % kZcLanes];
+            std::unique_lock<std::mutex> t(cand.mu, std::try_to_lock);
+            if (t.owns_lock()) {
+                llk = std::move(t);
+                ln = &cand;
+            }
+        }
+        if (!ln) {
+            ln = &ev->zc[start % kZcLanes];
+            llk = std::unique_lock<std::mutex>(ln->mu);
+        }
         const int pbz = packed_bytes(ev->domain);
-        std::memcpy(ev->zc_in, packed, static_cast<size_t>(n) * pbz);
-        int rc = launch(ev, ev->zc_in_dev, n, ev->zc_out_dev, nullptr, ev->stream[0]);
+        std::memcpy(ln->in, packed, static_cast<size_t>(n) * pbz);
+        int rc = launch(ev, ln->in_dev, n, ln->out_dev, nullptr, ln->st);
         if (rc == BIDA_OK) {
-            const cudaError_t e = cudaStreamSynchronize(ev->stream[0]);
+            const cudaError_t e = cudaStreamSynchronize(ln->st);
             if (e != cudaSuccess)
                 rc = fail(BIDA_ERR_CUDA, std::string("evaluate: ") + cudaGetErrorString(e));
         }
@@ -509,9 +545,10 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
             collect_errors(ev);
             return rc;
         }
-        std::memcpy(h_out, ev->zc_out, static_cast<size_t>(n) * 4);
+        std::memcpy(h_out, ln->out, static_cast<size_t>(n) * 4);
         return collect_errors(ev);
     }
+    std::lock_guard<std::mutex> lk(ev->mu);
     if (int rc = ensure_slots(ev, n)) {
         std::fill(h_out, h_out + n, 0);
         return rc;
@@ -646,6 +683,8 @@ int bida_gpu_attach_pdb(bida_gpu_evaluator *ev, const uint8_t *pattern, int patt
     if (!ev)
         return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL evaluator");
     std::lock_guard<std::mutex> lk(ev->mu);
+    static_assert(kZcLanes == 4, "lock every zero-copy lane");
+    std::scoped_lock lanes(ev->zc[0].mu, ev->zc[1].mu, ev->zc[2].mu, ev->zc[3].mu);
     CUDA_TRY(cudaSetDevice(ev->device));
     if (mode == BIDA_PDB_OFF) {
         if (ev->d_pdb)
