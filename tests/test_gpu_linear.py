@@ -206,3 +206,29 @@ def test_extreme_logit_scales(orc, scale, C):
         with bida.LinearModelBackend("rc", W, C, q) as be:
             h = be.evaluate(packed)
         assert (h == orc.linear_evaluate(RC, W, q, packed)).all(), q
+
+
+def test_concurrent_callers_on_one_handle(orc):
+    """The C-ABI handle is re-entrant: 8 host threads hammer one
+    handle with small (zero-copy lane) and large (staged slot) batches at
+    once; every result is bit-exact against the oracle."""
+    import threading
+
+    rng = np.random.default_rng(77)
+    W = rng.uniform(-0.1, 0.1, (2, 21, 480)).astype(np.float32)
+    batches = [bida.random_walks("rc", n, 0, 30, seed=100 + i)
+               for i, n in enumerate([1, 7, 513, 4096, 32768, 40000, 3000, 1 << 16] * 2)]
+    want = [orc.linear_evaluate(RC, W, 0.5, b) for b in batches]
+    got = [None] * len(batches)
+    with bida.LinearModelBackend("rc", W, 21, 0.5) as be:
+        def work(t):
+            for _ in range(3):
+                for i in range(t, len(batches), 8):
+                    got[i] = be.evaluate(batches[i])
+        ths = [threading.Thread(target=work, args=(t,)) for t in range(8)]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+    for g_, w_ in zip(got, want):
+        assert (g_ == w_).all()
