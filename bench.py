@@ -331,7 +331,11 @@ def cpu_rate(wl, seconds_target, threads, seed=7):
 SEARCH_WALKS = "1:15:15:2508"  # one walk-15 Rubik's scramble (configs[1]: walks 14-16)
 
 
-def search_leg(wl, seconds, threads, cpu: bool):
+# ring-evaluator search leg configuration (profiles/r1_search_ring.jsonl sweep)
+RING_SEARCH = {"evaluators": 2, "agents": 2, "batch": 16384, "timeout_us": 25}
+
+
+def search_leg(wl, seconds, threads, cpu: bool, ring: dict | None = None):
     """Batch IDA* nodes/s (BASELINE metric, second half): the reference's own
     batch_idastar (search.hpp:101-237) over a walk-15 Rubik's scramble, the
     workload's BMLP1 network evaluated for every generated node, search guided
@@ -339,7 +343,10 @@ def search_leg(wl, seconds, threads, cpu: bool):
     GPU: tools/bin/bida_search with 8 GpuBackend evaluators (network + PDB in
     the device readout).  CPU (cpu=True, baseline leg only): the test build
     tests/cpp/bin/search_parity with the oracle's CPU network, one evaluator
-    per searcher thread."""
+    per searcher thread.  ring={"evaluators": E, "agents": K, "batch": B,
+    "timeout_us": t}: tools/bin/bida_search_ring, the same search with the
+    reference's Evaluator internals replaced by the ring evaluator (SURVEY
+    §8(f) row 1, include/bida_ring_evaluator.hpp)."""
     from paper_2507_11916_b200.models import make_bmlp1
 
     if wl["domain"] != "rc" or wl["kind"] != "mlp":
@@ -350,6 +357,10 @@ def search_leg(wl, seconds, threads, cpu: bool):
     if cpu:
         exe = os.path.join(ROOT, "tests", "cpp", "bin", "search_parity")
         extra = ["--mode", "cpu", "--evaluators", str(threads), "--work-num", "8", "--batch", "512", "--timeout-us", "200"]
+    elif ring:
+        exe = os.path.join(ROOT, "tools", "bin", "bida_search_ring")
+        extra = ["--mode", "gpu", "--gpu-pdb", "--evaluators", str(ring["evaluators"]), "--work-num", "128",
+                 "--batch", str(ring["batch"]), "--timeout-us", str(ring["timeout_us"])]
     else:
         exe = os.path.join(ROOT, "tools", "bin", "bida_search")
         extra = ["--mode", "gpu", "--gpu-pdb", "--evaluators", "8", "--work-num", "128", "--batch", "16384",
@@ -358,7 +369,8 @@ def search_leg(wl, seconds, threads, cpu: bool):
         return {"unavailable": f"{exe} not built"}
     cmd = [exe, "--domain", "rc", "--walks", SEARCH_WALKS, "--model", "mlp:" + model, "--q", str(wl["q"]),
            "--table1-pdb", "5", "--threads", str(threads), "--time-limit", str(seconds), *extra]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    env = {**os.environ, "BIDA_EVAL_AGENTS": str(ring["agents"])} if ring else None
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     os.unlink(model)
     rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
     if out.returncode or not rows:
@@ -366,7 +378,9 @@ def search_leg(wl, seconds, threads, cpu: bool):
     r = rows[0]
     return {"value": r["nodes_per_s"], "unit": "nodes/s", "evals_per_s": r["evals_per_s"],
             "generated": r["generated"], "wall_s": r["wall_s"], "status": r["status"], "mean_batch": r["mean_batch"],
-            "threads": threads, "evaluators": r["evaluators"], "work_num": r["work_num"], "timeout_us": r["timeout_us"]}
+            "threads": threads, "evaluators": r["evaluators"], "work_num": r["work_num"], "timeout_us": r["timeout_us"],
+            "batch": r["batch"], "evaluator_impl": r.get("evaluator_impl", "reference"),
+            **({"agents": ring["agents"]} if ring else {})}
 
 
 def host_cores():
@@ -531,6 +545,11 @@ def main():
                                           "sample": f"{cb['wall_s']:.0f} s of the same search, oracle BMLP1 on "
                                                     f"{threads} CPU evaluator threads"}
             line["search"] = sr
+        rr = search_leg(wl, args.search_seconds, threads, cpu=False, ring=RING_SEARCH)
+        if rr is not None:
+            line["search_ring"] = {"metric": "batch_idastar_nodes_per_s", **rr,
+                                   "config": {**sr["config"], "evaluator": "ring evaluator (SURVEY 8(f) row 1): "
+                                              "lock-free submit ring, K agents per evaluator"}} if sr else rr
     print(json.dumps(line), flush=True)
 
 

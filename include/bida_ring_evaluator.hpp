@@ -248,7 +248,13 @@ private:
                     due = true;
                 } else {
                     lk.unlock();
-                    std::this_thread::sleep_for(std::chrono::nanoseconds(std::min<std::int64_t>(wait_ns, 20000)));
+                    // sleep_for rounds up to the timer slack (~50 us): below
+                    // that, re-check between yields so a filling batch or a
+                    // short deadline is seen on time
+                    if (wait_ns < 200000)
+                        std::this_thread::yield();
+                    else
+                        std::this_thread::sleep_for(std::chrono::microseconds(100));
                     continue;
                 }
             } else if (!due) {
