@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <climits>
 #include <cstdint>
 #include <cstdlib>
 #include <memory>
@@ -62,6 +63,17 @@ inline int default_agents() {
     const int k = s ? std::atoi(s) : 2;
     return std::clamp(k, 1, 16);
 }
+inline int default_shards() {
+    const char *s = std::getenv("BIDA_EVAL_SHARDS");
+    const int k = s ? std::atoi(s) : 4;
+    return std::clamp(k, 1, 64);
+}
+// a small per-thread index, so a searcher thread keeps submitting to one shard
+inline std::size_t thread_slot() {
+    static std::atomic<std::size_t> next{0};
+    thread_local const std::size_t mine = next.fetch_add(1, std::memory_order_relaxed);
+    return mine;
+}
 inline void relax(unsigned &spins) {
     if (++spins < 64) {
 #if defined(__x86_64__)
@@ -77,22 +89,28 @@ template <class D>
 class Evaluator {
 public:
     Evaluator(std::unique_ptr<EvaluatorBackend<D>> backend, std::size_t capacity, std::int64_t timeout_us,
-              bool immediate = false, int agents = ring_detail::default_agents())
+              bool immediate = false, int agents = ring_detail::default_agents(),
+              int shards = ring_detail::default_shards())
         : backend_(std::move(backend)), capacity_(capacity), timeout_us_(timeout_us), immediate_(immediate) {
         if (capacity_ == 0)
             throw std::invalid_argument("Evaluator: capacity must be >= 1");
+        nshards_ = static_cast<std::size_t>(shards);
         std::size_t r = 4096;
-        while (r < 8 * capacity_)
+        while (r * nshards_ < 8 * capacity_)
             r <<= 1;
         ring_size_ = r;
         mask_ = r - 1;
-        items_ = std::make_unique<BatchItem<D>[]>(r);
-        meta_ = std::make_unique<Meta[]>(r);
-        for (std::size_t i = 0; i < r; ++i)
-            meta_[i].seq.store(i, std::memory_order_relaxed);
-        // producers wake agents when they see the queue go nonempty or cross a
-        // capacity multiple; out-of-order publication is covered by a window
-        wake_window_ = std::max<std::uint64_t>(64, 2 * std::thread::hardware_concurrency());
+        shards_ = std::make_unique<Shard[]>(nshards_);
+        for (std::size_t k = 0; k < nshards_; ++k) {
+            Shard &sh = shards_[k];
+            sh.items = std::make_unique<BatchItem<D>[]>(r);
+            sh.meta = std::make_unique<Meta[]>(r);
+            for (std::size_t i = 0; i < r; ++i)
+                sh.meta[i].seq.store(i, std::memory_order_relaxed);
+        }
+        // a producer wakes the agents when its shard goes nonempty or crosses
+        // a multiple of capacity / shards (the agents then check the total)
+        wake_step_ = std::max<std::uint64_t>(1, capacity_ / nshards_);
         if (!immediate_)
             for (int k = 0; k < agents; ++k)
                 agents_.emplace_back([this] { agent_loop(); });
@@ -110,26 +128,28 @@ public:
             std::int32_t v = 0;
             backend_->evaluate(std::span<const BatchItem<D>>(&item, 1), std::span<std::int32_t>(&v, 1));
             resolve(*t, v);
-            submitted_.fetch_add(1, std::memory_order_relaxed);
+            immediate_submitted_.fetch_add(1, std::memory_order_relaxed);
             return t;
         }
         if (closed_.load(std::memory_order_acquire))
             throw std::runtime_error("Evaluator: submission after shutdown");
-        const std::uint64_t pos = tail_.fetch_add(1, std::memory_order_acq_rel);
-        Meta &m = meta_[pos & mask_];
+        // each searcher thread stays on one shard: the tail it bumps is
+        // shared with ~threads/shards others instead of with every thread
+        Shard &sh = shards_[ring_detail::thread_slot() % nshards_];
+        const std::uint64_t pos = sh.tail.fetch_add(1, std::memory_order_acq_rel);
+        Meta &m = sh.meta[pos & mask_];
         unsigned spins = 0;
-        while (m.seq.load(std::memory_order_acquire) != pos) // ring full: wait for the lap to drain
+        while (m.seq.load(std::memory_order_acquire) != pos) // shard full: wait for the lap to drain
             ring_detail::relax(spins);
-        BatchItem<D> &it = items_[pos & mask_];
+        BatchItem<D> &it = sh.items[pos & mask_];
         it.ticket = t;
         it.state = state;
         it.features = std::move(features);
         if (timeout_us_ > 0)
             m.t_ns = ring_detail::now_ns();
         m.seq.store(pos + 1, std::memory_order_seq_cst);
-        submitted_.fetch_add(1, std::memory_order_relaxed);
-        const std::uint64_t depth = pos + 1 - head_.load(std::memory_order_seq_cst);
-        if (depth == 1 || (depth >= capacity_ && depth - capacity_ < wake_window_))
+        const std::uint64_t depth = pos + 1 - sh.head.load(std::memory_order_seq_cst);
+        if (depth == 1 || (depth <= ring_size_ && depth % wake_step_ == 0))
             wake();
         return t;
     }
@@ -167,7 +187,7 @@ public:
 
     // Flush the pending items even though no batch is full.
     void request_flush() {
-        if (tail_.load(std::memory_order_acquire) == head_.load(std::memory_order_acquire))
+        if (!pending())
             return;
         if (!force_.exchange(true, std::memory_order_acq_rel))
             wake();
@@ -188,16 +208,40 @@ public:
         return stats_;
     }
 
-    std::uint64_t submitted() const { return submitted_.load(std::memory_order_relaxed); }
+    std::uint64_t submitted() const {
+        std::uint64_t n = immediate_submitted_.load(std::memory_order_relaxed);
+        for (std::size_t k = 0; k < nshards_; ++k)
+            n += shards_[k].tail.load(std::memory_order_relaxed);
+        return n;
+    }
     std::uint64_t resolved() const { return resolved_.load(std::memory_order_relaxed); }
     std::uint64_t double_resolutions() const { return double_resolved_.load(std::memory_order_relaxed); }
     std::size_t agent_count() const { return agents_.size(); }
+    std::size_t shard_count() const { return nshards_; }
 
 private:
     struct Meta {
         std::atomic<std::uint64_t> seq{0}; // == pos: free for lap pos; == pos+1: published
         std::int64_t t_ns = 0;             // submit time (timeout > 0 only)
     };
+    struct Shard {
+        alignas(64) std::atomic<std::uint64_t> tail{0}; // next position producers claim
+        alignas(64) std::atomic<std::uint64_t> head{0}; // next position agents claim
+        std::unique_ptr<BatchItem<D>[]> items;
+        std::unique_ptr<Meta[]> meta;
+    };
+    struct Range {
+        std::size_t shard;
+        std::uint64_t h;
+        std::size_t n;
+    };
+
+    bool pending() const {
+        for (std::size_t k = 0; k < nshards_; ++k)
+            if (shards_[k].tail.load(std::memory_order_acquire) != shards_[k].head.load(std::memory_order_acquire))
+                return true;
+        return false;
+    }
 
     void wake() {
         epoch_.fetch_add(1, std::memory_order_seq_cst);
@@ -207,28 +251,46 @@ private:
     void resolve(TicketSlot &t, std::int32_t v) {
         if (t.value.exchange(v, std::memory_order_release) != -1)
             double_resolved_.fetch_add(1, std::memory_order_relaxed);
-        resolved_.fetch_add(1, std::memory_order_relaxed);
     }
 
-    // published items contiguous from h, at most capacity
-    std::size_t published_from(std::uint64_t h) const {
+    // published items contiguous from the shard head, at most `limit`
+    std::size_t published_from(const Shard &sh, std::uint64_t h, std::size_t limit) const {
         std::size_t n = 0;
-        while (n < capacity_ && meta_[(h + n) & mask_].seq.load(std::memory_order_acquire) == h + n + 1)
+        while (n < limit && sh.meta[(h + n) & mask_].seq.load(std::memory_order_acquire) == h + n + 1)
             ++n;
         return n;
     }
 
     void agent_loop() {
-        std::vector<BatchItem<D>> scratch; // only for batches that wrap the ring
+        std::vector<BatchItem<D>> scratch; // batches spanning shards or a ring end
         std::vector<std::int32_t> vals;
+        std::vector<Range> ranges;
+        std::size_t rot = 0;
         for (;;) {
             const std::uint32_t e = epoch_.load(std::memory_order_seq_cst);
             std::unique_lock<std::mutex> lk(claim_m_);
-            const std::uint64_t h = head_.load(std::memory_order_relaxed);
-            const std::size_t n = published_from(h);
+            // published work per shard, starting from a rotating shard so no
+            // shard starves when the total exceeds one batch
+            ranges.clear();
+            std::size_t n = 0;
+            std::int64_t oldest = INT64_MAX;
+            bool drained = true;
+            for (std::size_t j = 0; j < nshards_ && n < capacity_; ++j) {
+                const std::size_t k = (rot + j) % nshards_;
+                Shard &sh = shards_[k];
+                const std::uint64_t h = sh.head.load(std::memory_order_relaxed);
+                const std::size_t c = published_from(sh, h, capacity_ - n);
+                if (sh.tail.load(std::memory_order_acquire) != h + c)
+                    drained = false;
+                if (c) {
+                    ranges.push_back({k, h, c});
+                    n += c;
+                    if (timeout_us_ > 0)
+                        oldest = std::min(oldest, sh.meta[h & mask_].t_ns);
+                }
+            }
             const bool closed = closed_.load(std::memory_order_acquire);
             if (n == 0) {
-                const bool drained = tail_.load(std::memory_order_acquire) == h;
                 lk.unlock();
                 if (closed && drained)
                     return;
@@ -243,7 +305,7 @@ private:
             const bool force = force_.load(std::memory_order_acquire);
             bool due = full || force || closed || timeout_us_ == 0;
             if (!due && timeout_us_ > 0) {
-                const std::int64_t wait_ns = meta_[h & mask_].t_ns + timeout_us_ * 1000 - ring_detail::now_ns();
+                const std::int64_t wait_ns = oldest + timeout_us_ * 1000 - ring_detail::now_ns();
                 if (wait_ns <= 0) {
                     due = true;
                 } else {
@@ -258,44 +320,56 @@ private:
                     continue;
                 }
             } else if (!due) {
+                // timeout < 0, partial batch: producers wake us at per-shard
+                // steps, which need not coincide with the total reaching
+                // capacity, so re-check on a short sleep as well
                 lk.unlock();
-                epoch_.wait(e, std::memory_order_seq_cst);
+                std::this_thread::sleep_for(std::chrono::microseconds(50));
                 continue;
             }
-            head_.store(h + n, std::memory_order_seq_cst);
+            for (const Range &r : ranges)
+                shards_[r.shard].head.store(r.h + r.n, std::memory_order_seq_cst);
+            rot = (ranges.back().shard + 1) % nshards_;
             const bool forced_partial = force && !full;
             if (force)
                 force_.store(false, std::memory_order_release);
             lk.unlock();
             // another agent may proceed with the next range right away
-            if (tail_.load(std::memory_order_acquire) != h + n)
+            if (!drained || pending())
                 wake();
-            process(h, n, forced_partial, scratch, vals);
+            process(ranges, n, forced_partial, scratch, vals);
         }
     }
 
-    void process(std::uint64_t h, std::size_t n, bool forced_partial, std::vector<BatchItem<D>> &scratch,
-                 std::vector<std::int32_t> &vals) {
+    void process(const std::vector<Range> &ranges, std::size_t n, bool forced_partial,
+                 std::vector<BatchItem<D>> &scratch, std::vector<std::int32_t> &vals) {
         vals.assign(n, 0);
-        const std::size_t first = h & mask_;
-        const bool wraps = first + n > ring_size_;
-        if (!wraps) {
-            backend_->evaluate(std::span<const BatchItem<D>>(&items_[first], n), vals);
+        const Range &r0 = ranges.front();
+        const bool in_place = ranges.size() == 1 && (r0.h & mask_) + r0.n <= ring_size_;
+        if (in_place) {
+            Shard &sh = shards_[r0.shard];
+            backend_->evaluate(std::span<const BatchItem<D>>(&sh.items[r0.h & mask_], n), vals);
         } else {
             scratch.clear();
-            for (std::size_t i = 0; i < n; ++i)
-                scratch.push_back(std::move(items_[(h + i) & mask_]));
+            for (const Range &r : ranges)
+                for (std::size_t i = 0; i < r.n; ++i)
+                    scratch.push_back(std::move(shards_[r.shard].items[(r.h + i) & mask_]));
             backend_->evaluate(std::span<const BatchItem<D>>(scratch), vals);
         }
-        for (std::size_t i = 0; i < n; ++i) {
-            BatchItem<D> &it = wraps ? scratch[i] : items_[(h + i) & mask_];
-            resolve(*it.ticket, vals[i]);
-            it.ticket.reset();
-            if (!it.features.empty())
-                FeatureVector().swap(it.features);
+        std::size_t o = 0;
+        for (const Range &r : ranges) {
+            Shard &sh = shards_[r.shard];
+            for (std::size_t i = 0; i < r.n; ++i, ++o) {
+                BatchItem<D> &it = in_place ? sh.items[(r.h + i) & mask_] : scratch[o];
+                resolve(*it.ticket, vals[o]);
+                it.ticket.reset();
+                if (!it.features.empty())
+                    FeatureVector().swap(it.features);
+            }
+            for (std::size_t i = 0; i < r.n; ++i)
+                sh.meta[(r.h + i) & mask_].seq.store(r.h + i + ring_size_, std::memory_order_release);
         }
-        for (std::size_t i = 0; i < n; ++i)
-            meta_[(h + i) & mask_].seq.store(h + i + ring_size_, std::memory_order_release);
+        resolved_.fetch_add(n, std::memory_order_relaxed);
         std::lock_guard<std::mutex> slk(stats_m_);
         stats_.record_batch(n);
         if (forced_partial)
@@ -307,13 +381,11 @@ private:
     std::int64_t timeout_us_;
     bool immediate_;
 
-    std::size_t ring_size_ = 0;
+    std::size_t nshards_ = 1;
+    std::size_t ring_size_ = 0; // per shard
     std::uint64_t mask_ = 0;
-    std::uint64_t wake_window_ = 64;
-    std::unique_ptr<BatchItem<D>[]> items_;
-    std::unique_ptr<Meta[]> meta_;
-    alignas(64) std::atomic<std::uint64_t> tail_{0};
-    alignas(64) std::atomic<std::uint64_t> head_{0};
+    std::uint64_t wake_step_ = 1;
+    std::unique_ptr<Shard[]> shards_;
     alignas(64) std::atomic<std::uint32_t> epoch_{0};
     std::atomic<bool> force_{false};
     std::atomic<bool> closed_{false};
@@ -323,7 +395,7 @@ private:
     mutable std::mutex stats_m_;
     SearchStats stats_;
 
-    std::atomic<std::uint64_t> submitted_{0};
+    std::atomic<std::uint64_t> immediate_submitted_{0};
     std::atomic<std::uint64_t> resolved_{0};
     std::atomic<std::uint64_t> double_resolved_{0};
 };

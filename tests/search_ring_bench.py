@@ -1,7 +1,7 @@
 """SURVEY §8(f) row 1 measurement on one B200: Batch IDA* nodes/s with the
 reference's Evaluator (tools/bin/bida_search) vs the ring evaluator
 (tools/bin/bida_search_ring), both with GpuBackend (network + PDB on the
-device), swept over evaluators per GPU and agents per evaluator.  Rubik's
+device), swept over evaluators per GPU and submit-ring shards per evaluator.  Rubik's
 walk-15, Table-1 mode, BMLP1 480-128-128-21.  Not a pytest test; -> profiles/."""
 import json
 import os
@@ -20,19 +20,19 @@ common = ["--domain", "rc", "--walks", "1:15:15:2508", "--model", "mlp:" + model
           "--time-limit", secs, "--mode", "gpu", "--gpu-pdb", "--work-num", "128", "--threads", str(ncpu)]
 runs = []
 for E in (1, 2, 8):
-    for B, t in ((16384, 25), (4096, 0)):
-        runs.append(("reference", "bida_search", E, 1, B, t))
-        for K in (2, 4):
-            runs.append(("ring", "bida_search_ring", E, K, B, t))
-for impl, exe, E, K, B, t in runs:
+    runs.append(("reference", "bida_search", E, 1, 1, 16384, 25))
+    for S in (1, 4, 8):
+        runs.append(("ring", "bida_search_ring", E, 2, S, 16384, 25))
+    runs.append(("ring", "bida_search_ring", E, 2, 4, 4096, 0))
+for impl, exe, E, K, S, B, t in runs:
     out = subprocess.run([os.path.join(ROOT, "tools", "bin", exe), *common, "--evaluators", str(E), "--batch", str(B),
                           "--timeout-us", str(t)], capture_output=True, text=True, timeout=600,
-                         env={**os.environ, "BIDA_EVAL_AGENTS": str(K)})
+                         env={**os.environ, "BIDA_EVAL_AGENTS": str(K), "BIDA_EVAL_SHARDS": str(S)})
     rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
     if out.returncode or not rows:
-        print(json.dumps({"impl": impl, "evaluators": E, "agents": K, "error": out.stderr[-300:]}), flush=True)
+        print(json.dumps({"impl": impl, "evaluators": E, "agents": K, "shards": S, "error": out.stderr[-300:]}), flush=True)
         continue
     r = rows[0]
     r.pop("iterations", None)
-    r.update(impl=impl, agents=K, host_threads=ncpu)
+    r.update(impl=impl, agents=K, shards=S, host_threads=ncpu)
     print(json.dumps(r), flush=True)
