@@ -72,13 +72,15 @@ RING = os.path.join(ROOT, "tools", "bin", "bida_search_ring")
 
 
 @pytest.mark.skipif(not os.path.exists(RING), reason="tools/bin/bida_search_ring not built")
-@pytest.mark.parametrize("timeout_us", ["200", "0", "-1"])
-def test_ring_evaluator_matches_reference_evaluator(tmp_path, man3, timeout_us):
+@pytest.mark.parametrize("timeout_us,agents,shards", [("200", "2", "4"), ("0", "2", "4"), ("-1", "2", "4"),
+                                                      ("200", "3", "3"), ("-1", "1", "1"), ("0", "4", "8")])
+def test_ring_evaluator_matches_reference_evaluator(tmp_path, man3, timeout_us, agents, shards):
     """the same batch_idastar with the reference's Evaluator
     (batch_eval.hpp:193-381) and with the ring evaluator (include/
     bida_ring_evaluator.hpp) over the reference's CPU LinearModelBackend:
     identical costs, threshold histories and non-final per-iteration counts,
-    under each flush policy (timeout > 0, == 0, < 0 = full or forced only)."""
+    under each flush policy (timeout > 0, == 0, < 0 = full or forced only)
+    and several agent / submit-shard counts."""
     g = np.load(os.path.join(ROOT, "tests", "golden", "instances.npz"))
     inst = tmp_path / "stp8.txt"
     inst.write_text("\n".join("stp 3 " + " ".join(str((int(v) >> (4 * c)) & 15) for c in range(9))
@@ -87,7 +89,8 @@ def test_ring_evaluator_matches_reference_evaluator(tmp_path, man3, timeout_us):
             "--threads", "4", "--work-num", "4", "--batch", "32", "--timeout-us", timeout_us]
     rc, ref, err = run(args)
     assert rc == 0, err
-    out = subprocess.run([RING, *args], capture_output=True, text=True, timeout=300)
+    out = subprocess.run([RING, *args], capture_output=True, text=True, timeout=300,
+                         env={**os.environ, "BIDA_EVAL_AGENTS": agents, "BIDA_EVAL_SHARDS": shards})
     assert out.returncode == 0, out.stderr
     ring = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(ref) == len(ring) == 40
