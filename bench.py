@@ -332,9 +332,10 @@ SEARCH_WALKS = "1:15:15:2508"  # one walk-15 Rubik's scramble (configs[1]: walks
 
 
 # ring-evaluator search leg configuration (profiles/r1_search_ring.jsonl sweep)
-# one evaluator (the per-evaluator ceiling the ring lifts) and eight (the best host-bound config)
-RING_SEARCH = [{"evaluators": 1, "agents": 2, "batch": 16384, "timeout_us": 25},
-               {"evaluators": 8, "agents": 2, "batch": 16384, "timeout_us": 25}]
+# one evaluator (the per-evaluator ceiling the ring lifts) and two (the best config measured,
+# profiles/r1_search_ring_shards.jsonl)
+RING_SEARCH = [{"evaluators": 1, "agents": 2, "shards": 8, "batch": 16384, "timeout_us": 25},
+               {"evaluators": 2, "agents": 2, "shards": 8, "batch": 16384, "timeout_us": 25}]
 
 
 def search_leg(wl, seconds, threads, cpu: bool, ring: dict | None = None):
@@ -371,7 +372,8 @@ def search_leg(wl, seconds, threads, cpu: bool, ring: dict | None = None):
         return {"unavailable": f"{exe} not built"}
     cmd = [exe, "--domain", "rc", "--walks", SEARCH_WALKS, "--model", "mlp:" + model, "--q", str(wl["q"]),
            "--table1-pdb", "5", "--threads", str(threads), "--time-limit", str(seconds), *extra]
-    env = {**os.environ, "BIDA_EVAL_AGENTS": str(ring["agents"])} if ring else None
+    env = {**os.environ, "BIDA_EVAL_AGENTS": str(ring["agents"]), "BIDA_EVAL_SHARDS": str(ring["shards"])} \
+        if ring else None
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     os.unlink(model)
     rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
@@ -382,7 +384,7 @@ def search_leg(wl, seconds, threads, cpu: bool, ring: dict | None = None):
             "generated": r["generated"], "wall_s": r["wall_s"], "status": r["status"], "mean_batch": r["mean_batch"],
             "threads": threads, "evaluators": r["evaluators"], "work_num": r["work_num"], "timeout_us": r["timeout_us"],
             "batch": r["batch"], "evaluator_impl": r.get("evaluator_impl", "reference"),
-            **({"agents": ring["agents"]} if ring else {})}
+            **({"agents": ring["agents"], "shards": ring["shards"]} if ring else {})}
 
 
 def host_cores():
@@ -553,7 +555,7 @@ def main():
             if rr is not None:
                 legs.append({"metric": "batch_idastar_nodes_per_s", **rr, "evaluator":
                              "ring evaluator (SURVEY 8(f) row 1, include/bida_ring_evaluator.hpp): lock-free "
-                             "submit ring, K agents per evaluator; same search, instance and model as 'search'"})
+                             "sharded submit ring, K agents per evaluator; same search, instance and model as 'search'"})
         if legs:
             line["search_ring"] = legs
     print(json.dumps(line), flush=True)

@@ -12,9 +12,11 @@
 // launch, copy out) is idle host time and caps one evaluator at ~1.9 M
 // nodes/s (profiles/r1_search_rc_gpu.jsonl).  Here:
 //
-//   * submissions go into a bounded multi-producer ring (one fetch_add on the
-//     tail, a per-slot sequence word publishes the item); no mutex, no
-//     vector growth, no notify per submit;
+//   * submissions go into bounded multi-producer rings, S shards per
+//     evaluator (default 8, env BIDA_EVAL_SHARDS; searcher thread i uses
+//     shard i mod S): one fetch_add on the shard tail, a per-slot sequence
+//     word publishes the item; no mutex, no vector growth, no notify per
+//     submit, no counter shared by every searcher;
 //   * K agents per evaluator (default 2, env BIDA_EVAL_AGENTS) claim
 //     contiguous published ranges under a short claim lock and run backend
 //     calls concurrently, so batch i+1 is staged and launched while batch i
@@ -65,7 +67,7 @@ inline int default_agents() {
 }
 inline int default_shards() {
     const char *s = std::getenv("BIDA_EVAL_SHARDS");
-    const int k = s ? std::atoi(s) : 4;
+    const int k = s ? std::atoi(s) : 8;
     return std::clamp(k, 1, 64);
 }
 // a small per-thread index, so a searcher thread keeps submitting to one shard
