@@ -133,6 +133,9 @@ public:
             immediate_submitted_.fetch_add(1, std::memory_order_relaxed);
             return t;
         }
+        // A submit that races close() itself (not a pattern the search uses:
+        // groups close after their searchers join) may land after the agents
+        // drained; the reference closes that window with its buffer mutex.
         if (closed_.load(std::memory_order_acquire))
             throw std::runtime_error("Evaluator: submission after shutdown");
         // each searcher thread stays on one shard: the tail it bumps is
