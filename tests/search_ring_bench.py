@@ -19,6 +19,21 @@ ncpu = len(os.sched_getaffinity(0))
 common = ["--domain", "rc", "--walks", "1:15:15:2508", "--model", "mlp:" + model, "--table1-pdb", "5",
           "--time-limit", secs, "--mode", "gpu", "--gpu-pdb", "--work-num", "128", "--threads", str(ncpu)]
 runs = []
+if len(sys.argv) > 2 and sys.argv[2] == "threads":
+    # config 5's CPU thread sweep with one ring evaluator (the one-evaluator-per-GPU mapping)
+    for n in sorted({2, 4, 8, 16, ncpu}):
+        common[common.index("--threads") + 1] = str(n)
+        for impl, exe, K, S in (("reference", "bida_search", 1, 1), ("ring", "bida_search_ring", 2, 8)):
+            out = subprocess.run([os.path.join(ROOT, "tools", "bin", exe), *common, "--evaluators", "1", "--batch",
+                                  "16384", "--timeout-us", "25"], capture_output=True, text=True, timeout=600,
+                                 env={**os.environ, "BIDA_EVAL_AGENTS": str(K), "BIDA_EVAL_SHARDS": str(S)})
+            for l in out.stdout.splitlines():
+                if l.startswith("{"):
+                    r = json.loads(l)
+                    r.pop("iterations", None)
+                    r.update(impl=impl, agents=K, shards=S, host_threads=ncpu)
+                    print(json.dumps(r), flush=True)
+    sys.exit(0)
 for E in (1, 2, 8):
     runs.append(("reference", "bida_search", E, 1, 1, 16384, 25))
     for S in (1, 4, 8):
