@@ -1,0 +1,187 @@
+// Evaluator semantics, restated from the reference's own unit tests
+// (/root/reference/proj/tests/test_batch_eval.cpp:35-118, 120-141, 243-268;
+// Catch2 is absent here, so plain checks).  Built twice by tests/cpp/Makefile:
+// against the reference's batch_eval.hpp (bin/evaluator_semantics_ref, the
+// control) and against the ring evaluator overlay (bin/evaluator_semantics_ring,
+// include/bida_ring_evaluator.hpp).  Exit 0 = every check passed.
+#include <array>
+#include <chrono>
+#include <cstdio>
+#include <random>
+#include <thread>
+#include <vector>
+
+#include "bida/batch_eval.hpp"
+#include "bida/heuristic.hpp"
+#include "bida/stp.hpp"
+
+using namespace bida;
+using D = TilePuzzle<3>;
+
+static int failures = 0;
+#define CHECK(c)                                                                \
+    do {                                                                        \
+        if (!(c)) {                                                             \
+            std::fprintf(stderr, "%s:%d: CHECK failed: %s\n", __FILE__, __LINE__, #c); \
+            ++failures;                                                         \
+        }                                                                       \
+    } while (0)
+
+namespace {
+D::State walk(std::mt19937_64 &rng, int steps = 30) {
+    D::State s = D::solved();
+    D::Action last = D::kNoAction;
+    for (int i = 0; i < steps; ++i) {
+        std::array<D::Action, 4> acts{};
+        const int n = D::actions(s, last, true, acts);
+        last = acts[static_cast<std::size_t>(std::uniform_int_distribution<int>(0, n - 1)(rng))];
+        s = D::apply(s, last);
+    }
+    return s;
+}
+std::shared_ptr<const Heuristic<D>> man() { return std::make_shared<ManhattanHeuristic<3>>(); }
+std::unique_ptr<EvaluatorBackend<D>> sim() { return std::make_unique<TableSimBackend<D>>(man()); }
+void wait_all(const std::vector<Ticket> &ts, double seconds) {
+    const auto end = std::chrono::steady_clock::now() + std::chrono::duration<double>(seconds);
+    for (const auto &t : ts)
+        while (poll(t) < 0 && std::chrono::steady_clock::now() < end)
+            std::this_thread::yield();
+}
+} // namespace
+
+int main() {
+    ManhattanHeuristic<3> mh;
+    { // a full buffer is exactly one flush, values equal direct lookups
+        Evaluator<D> ev(sim(), 8, -1);
+        std::mt19937_64 rng(1);
+        std::vector<D::State> ss;
+        std::vector<Ticket> ts;
+        for (int i = 0; i < 8; ++i) {
+            ss.push_back(walk(rng));
+            ts.push_back(ev.submit(ss.back(), {}));
+        }
+        wait_all(ts, 2);
+        for (int i = 0; i < 8; ++i)
+            CHECK(poll(ts[i]) == mh.lookup(ss[i]));
+        const SearchStats st = ev.stats_snapshot();
+        CHECK(st.batches == 1 && st.batch_items == 8 && st.max_batch_occupancy == 8);
+    }
+    { // timeout flushes a partial batch
+        Evaluator<D> ev(sim(), 1024, 2000);
+        const Ticket t = ev.submit(D::solved(), {});
+        wait_all({t}, 2);
+        CHECK(poll(t) == 0);
+        CHECK(ev.stats_snapshot().batches == 1);
+    }
+    { // no submissions, no flushes
+        Evaluator<D> ev(sim(), 4, 100);
+        std::this_thread::sleep_for(std::chrono::milliseconds(2));
+        CHECK(ev.stats_snapshot().batches == 0);
+    }
+    { // timeout disabled: flushes = submissions / capacity
+        const std::size_t B = 16;
+        Evaluator<D> ev(sim(), B, -1);
+        std::mt19937_64 rng(2);
+        std::vector<Ticket> ts;
+        for (std::size_t i = 0; i < 10 * B; ++i)
+            ts.push_back(ev.submit(walk(rng), {}));
+        wait_all(ts, 5);
+        const SearchStats st = ev.stats_snapshot();
+        CHECK(st.batches == 10 && st.batch_items == 10 * B && st.max_batch_occupancy == B);
+    }
+    { // close drains, then submissions throw
+        Evaluator<D> ev(sim(), 1024, -1);
+        std::mt19937_64 rng(3);
+        std::vector<Ticket> ts;
+        for (int i = 0; i < 37; ++i)
+            ts.push_back(ev.submit(walk(rng), {}));
+        ev.close();
+        for (const auto &t : ts)
+            CHECK(poll(t) >= 0);
+        bool threw = false;
+        try {
+            ev.submit(D::solved(), {});
+        } catch (const std::runtime_error &) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    { // request_flush forces one partial batch
+        Evaluator<D> ev(sim(), 1024, -1);
+        const Ticket t = ev.submit(D::solved(), {});
+        ev.request_flush();
+        wait_all({t}, 2);
+        CHECK(poll(t) == 0);
+        CHECK(ev.stats_snapshot().forced_flushes == 1);
+    }
+    { // group: evaluate_single, even routing
+        EvaluatorGroup<D> g = make_table_sim_group<D>(man(), 2, 8, 0);
+        CHECK(g.evaluate_single(D::solved()) == 0);
+        std::mt19937_64 rng(4);
+        for (int i = 0; i < 50; ++i) {
+            const D::State s = walk(rng);
+            CHECK(g.evaluate_single(s) == mh.lookup(s));
+        }
+        std::array<int, 2> load{};
+        for (int tid = 0; tid < 4; ++tid)
+            ++load[static_cast<std::size_t>(g.evaluator_of(tid))];
+        CHECK(load[0] == 2 && load[1] == 2);
+        g.close();
+    }
+    { // liveness under randomized schedules: 200 rounds of random capacity,
+      // timeout, bursts, kicks and mid-flight shutdowns
+        std::mt19937_64 rng(7);
+        std::uint64_t doubled = 0;
+        for (int round = 0; round < 200; ++round) {
+            const std::size_t B = 1 + rng() % 16;
+            const std::int64_t timeout = static_cast<std::int64_t>(rng() % 3) - 1;
+            Evaluator<D> ev(sim(), B, timeout);
+            std::vector<Ticket> ts;
+            const int count = static_cast<int>(rng() % 40);
+            for (int i = 0; i < count; ++i) {
+                ts.push_back(ev.submit(walk(rng, 6), {}));
+                if (rng() % 8 == 0)
+                    ev.request_flush();
+                if (rng() % 16 == 0)
+                    std::this_thread::yield();
+            }
+            ev.close();
+            for (const auto &t : ts)
+                CHECK(poll(t) >= 0);
+            CHECK(ev.submitted() == ev.resolved());
+            doubled += ev.double_resolutions();
+        }
+        CHECK(doubled == 0);
+    }
+    { // many producer threads into one evaluator (beyond the reference tests):
+      // every ticket resolved to its own state's value, none twice
+        Evaluator<D> ev(sim(), 64, 0);
+        std::vector<std::thread> th;
+        std::vector<std::vector<std::pair<D::State, Ticket>>> got(8);
+        for (int k = 0; k < 8; ++k)
+            th.emplace_back([&, k] {
+                std::mt19937_64 rng(100 + k);
+                for (int i = 0; i < 20000; ++i) {
+                    const D::State s = walk(rng, 8);
+                    got[k].emplace_back(s, ev.submit(s, {}));
+                }
+            });
+        for (auto &t : th)
+            t.join();
+        ev.close();
+        std::size_t n = 0;
+        for (auto &v : got)
+            for (auto &[s, t] : v) {
+                CHECK(poll(t) == mh.lookup(s));
+                ++n;
+            }
+        CHECK(n == 160000 && ev.submitted() == n && ev.resolved() == n && ev.double_resolutions() == 0);
+        CHECK(ev.stats_snapshot().batch_items == n);
+    }
+#ifdef BIDA_RING_EVALUATOR
+    std::printf("ring evaluator: %s\n", failures ? "FAILED" : "all checks passed");
+#else
+    std::printf("reference evaluator: %s\n", failures ? "FAILED" : "all checks passed");
+#endif
+    return failures ? 1 : 0;
+}

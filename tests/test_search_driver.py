@@ -119,3 +119,19 @@ def test_ring_evaluator_rc_tablesim_multi_evaluator():
     assert [r["status"] for r in ring] == ["solved"] * 3
     assert [r["cost"] for r in ring] == [r["cost"] for r in ref]
     assert [r["thresholds"] for r in ring] == [r["thresholds"] for r in ref]
+
+
+@pytest.mark.parametrize("impl", ["ref", "ring"])
+def test_evaluator_unit_semantics(impl):
+    """The reference's Evaluator unit tests (test_batch_eval.cpp:35-141, 243-268)
+    restated in tests/cpp/evaluator_semantics.cpp, run against the reference
+    header (control) and the ring evaluator: flush counts, timeout, forced
+    flush, close-drains-then-throws, routing, randomized liveness with
+    submitted == resolved and no double resolution, plus 8 concurrent
+    producers."""
+    exe = os.path.join(ROOT, "tests", "cpp", "bin", f"evaluator_semantics_{impl}")
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "all checks passed" in out.stdout
