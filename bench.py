@@ -332,9 +332,10 @@ SEARCH_WALKS = "1:15:15:2508"  # one walk-15 Rubik's scramble (configs[1]: walks
 
 
 # ring-evaluator search leg configuration (profiles/r1_search_ring.jsonl sweep)
-# one evaluator (the per-evaluator ceiling the ring lifts) and two (the best config measured,
+# one evaluator (the per-evaluator ceiling the ring lifts; K=4, S=16 was the best mean of
+# profiles/r1_search_ring_repeat.jsonl) and two at the header defaults (K=2, S=8;
 # profiles/r1_search_ring_shards.jsonl)
-RING_SEARCH = [{"evaluators": 1, "agents": 2, "shards": 8, "batch": 16384, "timeout_us": 25},
+RING_SEARCH = [{"evaluators": 1, "agents": 4, "shards": 16, "batch": 16384, "timeout_us": 25},
                {"evaluators": 2, "agents": 2, "shards": 8, "batch": 16384, "timeout_us": 25}]
 
 
