@@ -132,12 +132,31 @@ int bida_gpu_attach_pdb(bida_gpu_evaluator *ev, const uint8_t *pattern, int patt
 /* Same from a BPDB1 file written by PdbTable::save (pdb.hpp:78-96). */
 int bida_gpu_attach_pdb_file(bida_gpu_evaluator *ev, const char *path, int mode);
 
+/* PdbTable<D>::build(pattern, D::solved()) (pdb.hpp:30-64) as a level-
+ * synchronous breadth-first search on the GPU; the table is byte-identical to
+ * the reference's (BFS distances are unique).  `max_entries` (0 = the
+ * reference's default cap 2^28, pdb.hpp kDefaultPdbEntryCap) mirrors the
+ * reference's size check and message.  *n_entries is set before the capacity
+ * check, so a call with entries_out == NULL sizes the buffer. */
+int bida_gpu_pdb_build(int device, int domain, const uint8_t *pattern, int pattern_len, uint64_t max_entries,
+                       uint8_t *entries_out, uint64_t out_cap, uint64_t *n_entries, int *max_depth);
+/* Same, written to `path` in the BPDB1 format of PdbTable::save (pdb.hpp:78-96),
+ * so the reference's PdbTable::load reads it. */
+int bida_gpu_pdb_build_save(int device, int domain, const uint8_t *pattern, int pattern_len, const char *path);
+/* Builds the table on the evaluator's device and attaches it (no host copy). */
+int bida_gpu_attach_pdb_built(bida_gpu_evaluator *ev, const uint8_t *pattern, int pattern_len, int mode);
+
 int bida_gpu_info(const bida_gpu_evaluator *ev, bida_gpu_model_info *out);
 /* Diagnostics (MLP handles): record a clock64 timeline of CTA 0's warps into
  * the DEVICE buffer `dev_buf` (int64 [32 warps][bida_gpu_trace_slots()]) on every
  * subsequent launch; NULL switches it off. */
 int bida_gpu_debug_trace(bida_gpu_evaluator *ev, long long *dev_buf);
 int bida_gpu_trace_slots(void);
+/* Parity diagnostics: number of (state, member) readouts so far whose
+ * certified float32 softmax bound could not decide the class and that replayed
+ * the reference's float64 sequence (batch_eval.hpp:159-166,
+ * heuristic.hpp:95-120) instead.  Synchronous; counts completed work only. */
+int bida_gpu_exact_replays(bida_gpu_evaluator *ev, int64_t *out);
 /* Number of kernel launches issued by this handle so far (bench evidence). */
 int64_t bida_gpu_launch_count(const bida_gpu_evaluator *ev);
 int bida_gpu_destroy(bida_gpu_evaluator *ev);

@@ -231,6 +231,53 @@ int ref_linear_evaluate(int domain, const float *W, int E, int C, double q, cons
     });
 }
 
+// The reference's own LinearModelBackend::evaluate (score's softmax,
+// quantile_class, ensemble_min: batch_eval.hpp:98-105,148-168,
+// heuristic.hpp:95-126) applied to ARBITRARY per-(state, member, class)
+// logits of the form (double)acc * (double)scale, acc int32, scale float --
+// the BMLP1 output layer, which the reference does not have.
+//
+// score() computes sum_j (double)w[c][j] * (double)x[j] over F float
+// features.  For member m, class c we use two feature slots
+// j0 = 2(mC + c), j1 = j0 + 1 holding the split acc = hi + lo
+// (lo = acc & 4095, hi = acc - lo: both exact in float), and put the member's
+// scale at w_m[c][j0] = w_m[c][j1]; every other weight is 0.  Both products
+// are exact in double, the running sum is exactly 0 before j0, so the sum
+// rounds ONCE to round(acc * scale) == (double)acc * (double)scale, and the
+// later +-0.0 terms do not change it.  Needs 2*E*C <= F.
+int ref_readout_scaled_logits(int domain, const std::int32_t *acc, const float *scale, int E, int C,
+                              double q, std::int64_t n, std::int32_t *h_out, int threads) {
+    return dispatch(domain, [&](auto *d) {
+        using D = bare_t<decltype(d)>;
+        const int F = D::feature_length();
+        if (2 * E * C > F)
+            throw std::invalid_argument("ref_readout_scaled_logits: 2*E*C exceeds the feature length");
+        std::vector<std::vector<float>> w(static_cast<std::size_t>(E),
+                                          std::vector<float>(static_cast<std::size_t>(C) * F, 0.0f));
+        for (int m = 0; m < E; ++m)
+            for (int c = 0; c < C; ++c) {
+                const std::size_t j0 = static_cast<std::size_t>(2 * (m * C + c));
+                w[static_cast<std::size_t>(m)][static_cast<std::size_t>(c) * F + j0] = scale[m];
+                w[static_cast<std::size_t>(m)][static_cast<std::size_t>(c) * F + j0 + 1] = scale[m];
+            }
+        LinearModelBackend<D> backend(std::move(w), C, q);
+        std::vector<BatchItem<D>> items(static_cast<std::size_t>(n));
+        for (std::int64_t i = 0; i < n; ++i) {
+            FeatureVector &x = items[static_cast<std::size_t>(i)].features;
+            x.assign(static_cast<std::size_t>(F), 0.0f);
+            for (int m = 0; m < E; ++m)
+                for (int c = 0; c < C; ++c) {
+                    const std::int32_t a = acc[(i * E + m) * C + c];
+                    const std::int32_t lo = a & 4095;
+                    const std::size_t j0 = static_cast<std::size_t>(2 * (m * C + c));
+                    x[j0] = static_cast<float>(static_cast<std::int64_t>(a) - lo);
+                    x[j0 + 1] = static_cast<float>(lo);
+                }
+        }
+        return run_backend_mt<D>(backend, items, h_out, threads);
+    });
+}
+
 // Same, with the encode done once up front and timed separately by the
 // caller: returns an opaque prepared batch (for the CPU baseline, so the
 // timed region is LinearModelBackend::evaluate only, like the GPU's kernel).

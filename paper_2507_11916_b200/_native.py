@@ -57,9 +57,13 @@ EXPORTS = [
     "bida_gpu_stream_status",
     "bida_gpu_attach_pdb",
     "bida_gpu_attach_pdb_file",
+    "bida_gpu_attach_pdb_built",
+    "bida_gpu_pdb_build",
+    "bida_gpu_pdb_build_save",
     "bida_gpu_info",
     "bida_gpu_debug_trace",
     "bida_gpu_trace_slots",
+    "bida_gpu_exact_replays",
     "bida_gpu_launch_count",
     "bida_gpu_destroy",
 ]
@@ -99,8 +103,13 @@ def lib() -> C.CDLL:
     L.bida_gpu_stream_status.argtypes = [H]
     L.bida_gpu_attach_pdb.argtypes = [H, vp, i32, vp, C.c_uint64, i32]
     L.bida_gpu_attach_pdb_file.argtypes = [H, C.c_char_p, i32]
+    L.bida_gpu_attach_pdb_built.argtypes = [H, vp, i32, i32]
+    L.bida_gpu_pdb_build.argtypes = [i32, i32, vp, i32, C.c_uint64, vp, C.c_uint64, C.POINTER(C.c_uint64),
+                                     C.POINTER(i32)]
+    L.bida_gpu_pdb_build_save.argtypes = [i32, i32, vp, i32, C.c_char_p]
     L.bida_gpu_info.argtypes = [H, C.POINTER(ModelInfo)]
     L.bida_gpu_debug_trace.argtypes = [H, vp]
+    L.bida_gpu_exact_replays.argtypes = [H, C.POINTER(i64)]
     L.bida_gpu_launch_count.argtypes = [H]
     L.bida_gpu_launch_count.restype = i64
     L.bida_gpu_destroy.argtypes = [H]

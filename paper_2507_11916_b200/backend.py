@@ -105,6 +105,11 @@ class _GpuBackendBase:
         BPDB1 file via `path`."""
         m = {"off": _native.PDB_OFF, "min": _native.PDB_MIN, "replace": _native.PDB_REPLACE}[mode]
         L = _native.lib()
+        if entries is None and path is None and m != _native.PDB_OFF:
+            # build the table on this handle's device (bida_gpu_attach_pdb_built)
+            pat = np.ascontiguousarray(pattern, np.uint8)
+            _native.check(L.bida_gpu_attach_pdb_built(self._h, pat.ctypes.data_as(C.c_void_p), len(pat), m))
+            return
         if path is not None:
             _native.check(L.bida_gpu_attach_pdb_file(self._h, str(path).encode(), m))
             return
@@ -120,6 +125,13 @@ class _GpuBackendBase:
         out = _native.ModelInfo()
         _native.check(_native.lib().bida_gpu_info(self._h, C.byref(out)))
         return out
+
+    def exact_replays(self) -> int:
+        """(state, member) readouts so far that took the exact float64 replay
+        because the certified float32 bound could not decide (parity evidence)."""
+        v = C.c_int64(0)
+        _native.check(_native.lib().bida_gpu_exact_replays(self._h, C.byref(v)))
+        return int(v.value)
 
     def launch_count(self) -> int:
         return int(_native.lib().bida_gpu_launch_count(self._h))
@@ -219,3 +231,28 @@ class MlpModelBackend(_GpuBackendBase):
     def load(cls, domain, path: str, quantile: float, device: int = 0) -> "MlpModelBackend":
         with open(path, "rb") as f:
             return cls(domain, f.read(), quantile, device)
+
+
+def pdb_build(domain, pattern, device: int = 0, max_entries: int = 0) -> np.ndarray:
+    """PdbTable<D>::build(pattern, D::solved()) (pdb.hpp:30-64) on the GPU:
+    the entries (uint8; 0xFF unreachable), byte-identical to the reference's."""
+    L = _native.lib()
+    d = domain_id(domain)
+    pat = np.ascontiguousarray(pattern, np.uint8)
+    n = C.c_uint64(0)
+    rc = L.bida_gpu_pdb_build(device, d, pat.ctypes.data_as(C.c_void_p), len(pat), max_entries, None, 0,
+                              C.byref(n), None)
+    if rc != _native.BIDA_ERR_CAPACITY:
+        _native.check(rc)
+    out = np.empty(n.value, np.uint8)
+    depth = C.c_int(0)
+    _native.check(L.bida_gpu_pdb_build(device, d, pat.ctypes.data_as(C.c_void_p), len(pat), max_entries,
+                                       out.ctypes.data_as(C.c_void_p), n.value, C.byref(n), C.byref(depth)))
+    return out
+
+
+def pdb_build_save(domain, pattern, path: str, device: int = 0) -> None:
+    """Same, written as a BPDB1 file (PdbTable::save, pdb.hpp:78-96)."""
+    pat = np.ascontiguousarray(pattern, np.uint8)
+    _native.check(_native.lib().bida_gpu_pdb_build_save(device, domain_id(domain), pat.ctypes.data_as(C.c_void_p),
+                                                        len(pat), str(path).encode()))

@@ -19,6 +19,7 @@
 #include "../../include/bida_gpu.h"
 #include "common.cuh"
 #include "linear.cuh"
+#include "linear_thread.cuh"
 #include "mlp.cuh"
 #include "pdb.cuh"
 
@@ -57,11 +58,22 @@ int packed_bytes(int domain) {
 
 } // namespace
 
+namespace bida_gpu {
+std::string &last_error_ref() { return g_last_error; }
+int pdb_build_device(int domain, const uint8_t *pattern, int m, uint8_t **d_out, uint64_t *n_out);
+} // namespace bida_gpu
+
 // Host<->device pipelining of large batches: kSlots chunks of up to kMaxSlot
 // states in flight on kSlots streams, so the H2D copy of chunk i+1.. overlaps
 // the kernel of chunk i and the D2H of chunk i-1 (copy engines are full duplex).
 constexpr int kSlots = 4;
 constexpr int kZcLanes = 4;
+// Error channels: each zero-copy lane, the pipelined path and the device path
+// own kErrWords mapped words, so a bad state in one call is reported by that
+// call only (concurrent agents share a handle).
+constexpr int kChanPipe = kZcLanes;
+constexpr int kChanDevice = kZcLanes + 1;
+constexpr int kChannels = kZcLanes + 2;
 
 struct bida_gpu_evaluator {
     int kind = 0, domain = 0, F = 0, C = 0, E = 0, device = 0;
@@ -69,13 +81,18 @@ struct bida_gpu_evaluator {
     float uLo = 0.0f, uHi = 0.0f;
     int num_sms = 148;
 
-    // linear model
+    // linear model: thread-per-state kernel (linear_thread.cuh) when C <= 96
+    // and every weight is finite, else the warp-per-state kernel (linear.cuh)
+    bool lin_thread = false;
+    float *d_Wthr = nullptr;  // [E][F+1][Cp]
+    int Cp = 0, lin_cm = 0;
     float *d_Wt = nullptr;
     uint8_t *d_rowflag = nullptr;
     int any_rowflag = 0;
     int w_in_smem = 0;
     size_t lin_smem = 0;
     int lin_grid_cap = 0;
+    unsigned long long *d_replays = nullptr;  // readouts that took the exact float64 replay
 
     // MLP model
     MlpModel *mlp = nullptr;
@@ -90,7 +107,7 @@ struct bida_gpu_evaluator {
     int32_t *h_h[kSlots] = {};
     void *d_in[kSlots] = {};
     int32_t *d_h[kSlots] = {};
-    int *err_host = nullptr; // mapped pinned, kErrWords ints
+    int *err_host = nullptr; // mapped pinned, kChannels x kErrWords ints
     int *err_dev = nullptr;
     // small-batch zero-copy path: mapped pinned in/out read/written by the
     // kernel, kZcLanes independent lanes (own lock, stream and buffers) so
@@ -121,14 +138,10 @@ constexpr int64_t kZeroCopyMax = int64_t(1) << 15;
 
 template <int DOMAIN, int CS>
 int launch_linear_t(bida_gpu_evaluator *ev, const LinearArgs &a, cudaStream_t st) {
-    auto kern = linear_eval_kernel<DOMAIN, CS>;
-    if (ev->lin_smem > 48 * 1024)
-        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(ev->lin_smem)));
     const int64_t groups = (a.n + 31) / 32;
     const int64_t want = (groups + kLinearWarps - 1) / kLinearWarps;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, ev->lin_grid_cap)));
-    kern<<<grid, kLinearThreads, ev->lin_smem, st>>>(a);
+    linear_eval_kernel<DOMAIN, CS><<<grid, kLinearThreads, ev->lin_smem, st>>>(a);
     ev->launches.fetch_add(1, std::memory_order_relaxed);
     CUDA_TRY(cudaGetLastError());
     return BIDA_OK;
@@ -146,15 +159,74 @@ int launch_linear_d(bida_gpu_evaluator *ev, const LinearArgs &a, cudaStream_t st
     }
 }
 
+// Thread-per-state linear kernel (linear_thread.cuh): one instantiation per
+// (domain, class-slot count).
+template <int DOMAIN, int CM>
+void *linear_thread_fn() {
+    return reinterpret_cast<void *>(linear_thread_kernel<DOMAIN, CM>);
+}
+
+template <int DOMAIN>
+void *linear_thread_fn_cm(int cm) {
+    switch (cm) {
+    case 8: return linear_thread_fn<DOMAIN, 8>();
+    case 16: return linear_thread_fn<DOMAIN, 16>();
+    case 24: return linear_thread_fn<DOMAIN, 24>();
+    case 32: return linear_thread_fn<DOMAIN, 32>();
+    case 64: return linear_thread_fn<DOMAIN, 64>();
+    default: return linear_thread_fn<DOMAIN, 96>();
+    }
+}
+
+void *linear_thread_kernel_for(int domain, int cm) {
+    switch (domain) {
+    case BIDA_DOMAIN_STP2: return linear_thread_fn_cm<kSTP2>(cm);
+    case BIDA_DOMAIN_STP3: return linear_thread_fn_cm<kSTP3>(cm);
+    case BIDA_DOMAIN_STP4: return linear_thread_fn_cm<kSTP4>(cm);
+    default: return linear_thread_fn_cm<kRC>(cm);
+    }
+}
+
+int launch_linear_thread(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h,
+                         double *d_logits, cudaStream_t st, int *err) {
+    LinearThreadArgs a;
+    a.packed = d_packed;
+    a.n = n;
+    a.h_out = d_h;
+    a.logits_out = d_logits;
+    a.W = ev->d_Wthr;
+    a.E = ev->E;
+    a.C = ev->C;
+    a.Cp = ev->Cp;
+    a.rk.thr = ev->thr;
+    a.rk.uLo = ev->uLo;
+    a.rk.uHi = ev->uHi;
+    a.w_in_smem = ev->w_in_smem;
+    a.err = err;
+    a.replays = ev->d_replays;
+    a.pdb = ev->pdb;
+    if (!ev->d_pdb)
+        a.pdb.entries = nullptr;
+    const int64_t want = (n + kLinThreads - 1) / kLinThreads;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, ev->lin_grid_cap)));
+    void *args[] = {&a};
+    CUDA_TRY(cudaLaunchKernel(linear_thread_kernel_for(ev->domain, ev->lin_cm), dim3(grid), dim3(kLinThreads),
+                              args, ev->lin_smem, st));
+    ev->launches.fetch_add(1, std::memory_order_relaxed);
+    return BIDA_OK;
+}
+
 int launch(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h, double *d_logits,
-           cudaStream_t st) {
+           cudaStream_t st, int *err) {
     if (n <= 0)
         return BIDA_OK;
     if (ev->kind == BIDA_MODEL_MLP)
-        return mlp_launch(ev->mlp, ev->domain, d_packed, n, d_h, d_logits, ev->err_dev, st,
+        return mlp_launch(ev->mlp, ev->domain, d_packed, n, d_h, d_logits, err, ev->d_replays, st,
                           &ev->launches, ev->d_pdb ? &ev->pdb : nullptr)
                    ? fail(BIDA_ERR_CUDA, mlp_last_error())
                    : BIDA_OK;
+    if (ev->lin_thread)
+        return launch_linear_thread(ev, d_packed, n, d_h, d_logits, st, err);
     LinearArgs a;
     a.packed = d_packed;
     a.n = n;
@@ -169,7 +241,8 @@ int launch(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h
     a.uHi = ev->uHi;
     a.w_in_smem = ev->w_in_smem;
     a.any_rowflag = ev->any_rowflag;
-    a.err = ev->err_dev;
+    a.err = err;
+    a.replays = ev->d_replays;
     a.pdb = ev->pdb;
     if (!ev->d_pdb)
         a.pdb.entries = nullptr;
@@ -181,12 +254,16 @@ int launch(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h
     }
 }
 
-int collect_errors(bida_gpu_evaluator *ev) {
-    // one error word set per handle: with concurrent calls an error is
-    // reported by whichever call collects it first (errors mean corrupt
-    // states or non-finite logits, never a normal search)
-    std::lock_guard<std::mutex> lk(ev->err_mu);
-    volatile int *e = ev->err_host;
+int *chan_err(bida_gpu_evaluator *ev, int ch) { return ev->err_dev + ch * kErrWords; }
+
+// Decodes and clears one channel's error words.  Channels other than the
+// device path are owned by the call holding their lock; the device path's
+// words may be collected by any thread (bida_gpu_stream_status).
+int collect_errors(bida_gpu_evaluator *ev, int ch) {
+    std::unique_lock<std::mutex> lk(ev->err_mu, std::defer_lock);
+    if (ch == kChanDevice)
+        lk.lock();
+    volatile int *e = ev->err_host + ch * kErrWords;
     int rc = BIDA_OK;
     if (e[kErrState])
         rc = fail(BIDA_ERR_STATE, "packed state encodes a feature outside [0, F)");
@@ -238,9 +315,11 @@ int common_init(bida_gpu_evaluator *ev, int device) {
         CUDA_TRY(cudaStreamCreateWithFlags(&ev->stream[s], cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreateWithFlags(&ev->done[s], cudaEventDisableTiming));
     }
-    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&ev->err_host), kErrWords * sizeof(int),
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&ev->err_host), kChannels * kErrWords * sizeof(int),
                            cudaHostAllocMapped));
-    std::memset(ev->err_host, 0, kErrWords * sizeof(int));
+    std::memset(ev->err_host, 0, kChannels * kErrWords * sizeof(int));
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void **>(&ev->d_replays), sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemset(ev->d_replays, 0, sizeof(unsigned long long)));
     CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&ev->err_dev), ev->err_host, 0));
     for (auto &ln : ev->zc) {
         CUDA_TRY(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking));
@@ -273,6 +352,8 @@ void release(bida_gpu_evaluator *ev) {
         if (ln.st) cudaStreamDestroy(ln.st);
     }
     if (ev->d_Wt) cudaFree(ev->d_Wt);
+    if (ev->d_Wthr) cudaFree(ev->d_Wthr);
+    if (ev->d_replays) cudaFree(ev->d_replays);
     if (ev->d_rowflag) cudaFree(ev->d_rowflag);
     if (ev->d_pdb) cudaFree(ev->d_pdb);
     if (ev->mlp) mlp_destroy(ev->mlp);
@@ -360,7 +441,7 @@ int linear_create_impl(int device, int domain, const float *weights, int E, int 
         release(ev);
         return rc;
     };
-    {
+    if (C > kLinMaxClasses || ev->any_rowflag) {  // warp-per-state kernel's layout
         cudaError_t e = cudaMalloc(&ev->d_Wt, nw * sizeof(float));
         if (e == cudaSuccess)
             e = cudaMemcpy(ev->d_Wt, wt.data(), nw * sizeof(float), cudaMemcpyHostToDevice);
@@ -371,11 +452,70 @@ int linear_create_impl(int device, int domain, const float *weights, int E, int 
         if (e != cudaSuccess)
             return bail(fail(BIDA_ERR_CUDA, std::string("weight upload: ") + cudaGetErrorString(e)));
     }
+    if (C <= kLinMaxClasses && !ev->any_rowflag) {
+        // thread-per-state kernel: [E][F+1][Cp], zero pad columns and a zero row F
+        ev->lin_thread = true;
+        ev->Cp = (C + 3) & ~3;
+        ev->lin_cm = C <= 8 ? 8 : C <= 16 ? 16 : C <= 24 ? 24 : C <= 32 ? 32 : C <= 64 ? 64 : 96;
+        const size_t per = static_cast<size_t>(F + 1) * ev->Cp;
+        std::vector<float> w3(per * E, 0.0f);
+        for (int m = 0; m < E; ++m)
+            for (int c = 0; c < C; ++c)
+                for (int j = 0; j < F; ++j)
+                    w3[m * per + static_cast<size_t>(j) * ev->Cp + c] =
+                        weights[(static_cast<size_t>(m) * C + c) * F + j];
+        cudaError_t e = cudaMalloc(&ev->d_Wthr, w3.size() * sizeof(float));
+        if (e == cudaSuccess)
+            e = cudaMemcpy(ev->d_Wthr, w3.data(), w3.size() * sizeof(float), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess)
+            return bail(fail(BIDA_ERR_CUDA, std::string("weight upload: ") + cudaGetErrorString(e)));
+        const size_t wbytes = w3.size() * sizeof(float);
+        ev->w_in_smem = wbytes <= 200 * 1024 ? 1 : 0;
+        ev->lin_smem = ev->w_in_smem ? wbytes : 0;
+        void *fn = linear_thread_kernel_for(domain, ev->lin_cm);
+        if (ev->lin_smem > 48 * 1024) {
+            e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ev->lin_smem));
+            if (e != cudaSuccess)
+                return bail(fail(BIDA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e)));
+        }
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kLinThreads, ev->lin_smem);
+        if (e != cudaSuccess || per_sm < 1)
+            return bail(fail(BIDA_ERR_CUDA, "linear kernel does not fit on an SM"));
+        ev->lin_grid_cap = ev->num_sms * per_sm;
+        *out = ev;
+        return BIDA_OK;
+    }
     const int cpad = (C + 1) & ~1;
     const size_t extra = static_cast<size_t>(kLinearWarps) * cpad * 8 + kLinearWarps * 32 * 4;
     const size_t wbytes = (nw * 4 + 15) & ~size_t(15);
     ev->w_in_smem = (wbytes + extra <= 200 * 1024) ? 1 : 0;
     ev->lin_smem = (ev->w_in_smem ? wbytes : 0) + extra;
+    if (ev->lin_smem > 48 * 1024) {
+        // once per handle (the kernel instance depends on the domain and C)
+        cudaError_t e = cudaSuccess;
+        switch (domain) {
+#define BIDA_SET_ATTR(D)                                                                                   \
+    e = [&] {                                                                                              \
+        const int cs = (C + 31) / 32;                                                                      \
+        const void *fn = cs == 1   ? reinterpret_cast<const void *>(linear_eval_kernel<D, 1>)              \
+                         : cs == 2 ? reinterpret_cast<const void *>(linear_eval_kernel<D, 2>)              \
+                         : cs == 3 ? reinterpret_cast<const void *>(linear_eval_kernel<D, 3>)              \
+                         : cs == 4 ? reinterpret_cast<const void *>(linear_eval_kernel<D, 4>)              \
+                                   : reinterpret_cast<const void *>(linear_eval_kernel<D, 8>);             \
+        return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,                      \
+                                    static_cast<int>(ev->lin_smem));                                       \
+    }();                                                                                                   \
+    break;
+        case BIDA_DOMAIN_STP2: BIDA_SET_ATTR(kSTP2)
+        case BIDA_DOMAIN_STP3: BIDA_SET_ATTR(kSTP3)
+        case BIDA_DOMAIN_STP4: BIDA_SET_ATTR(kSTP4)
+        default: BIDA_SET_ATTR(kRC)
+#undef BIDA_SET_ATTR
+        }
+        if (e != cudaSuccess)
+            return bail(fail(BIDA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e)));
+    }
     // Resident CTAs per SM from the smem budget (228 KB/SM, 1 KB reserved per CTA).
     const size_t per_cta = ev->lin_smem + 1024;
     int per_sm = static_cast<int>(std::min<size_t>(8, (228 * 1024) / per_cta));
@@ -533,7 +673,8 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         }
         const int pbz = packed_bytes(ev->domain);
         std::memcpy(ln->in, packed, static_cast<size_t>(n) * pbz);
-        int rc = launch(ev, ln->in_dev, n, ln->out_dev, nullptr, ln->st);
+        const int ch = static_cast<int>(ln - ev->zc);
+        int rc = launch(ev, ln->in_dev, n, ln->out_dev, nullptr, ln->st, chan_err(ev, ch));
         if (rc == BIDA_OK) {
             const cudaError_t e = cudaStreamSynchronize(ln->st);
             if (e != cudaSuccess)
@@ -542,11 +683,11 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         ev->zc_calls.fetch_add(1, std::memory_order_relaxed);
         if (rc != BIDA_OK) {
             std::fill(h_out, h_out + n, 0);
-            collect_errors(ev);
+            collect_errors(ev, ch);
             return rc;
         }
         std::memcpy(h_out, ln->out, static_cast<size_t>(n) * 4);
-        return collect_errors(ev);
+        return collect_errors(ev, ch);
     }
     std::lock_guard<std::mutex> lk(ev->mu);
     if (int rc = ensure_slots(ev, n)) {
@@ -598,7 +739,7 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
             rc = fail(BIDA_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e));
             break;
         }
-        if ((rc = launch(ev, ev->d_in[slot], m, ev->d_h[slot], d_logits, st)))
+        if ((rc = launch(ev, ev->d_in[slot], m, ev->d_h[slot], d_logits, st, chan_err(ev, kChanPipe))))
             break;
         e = cudaMemcpyAsync(out_pinned ? static_cast<void *>(h_out + i0) : static_cast<void *>(ev->h_h[slot]),
                             ev->d_h[slot], m * 4, cudaMemcpyDeviceToHost, st);
@@ -634,10 +775,10 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         cudaFree(d_logits);
     if (rc != BIDA_OK) {
         std::fill(h_out, h_out + n, 0);
-        collect_errors(ev);
+        collect_errors(ev, kChanPipe);
         return rc;
     }
-    return collect_errors(ev);
+    return collect_errors(ev, kChanPipe);
 }
 
 int bida_gpu_evaluate(bida_gpu_evaluator *ev, const void *packed, int64_t n, int32_t *h_out) {
@@ -651,13 +792,13 @@ int bida_gpu_evaluate_device(bida_gpu_evaluator *ev, const void *d_packed, int64
     if (n < 0 || (n > 0 && (!d_packed || !d_h)))
         return fail(BIDA_ERR_INVALID_ARGUMENT, "bad batch arguments");
     CUDA_TRY(cudaSetDevice(ev->device));
-    return launch(ev, d_packed, n, d_h, d_logits, static_cast<cudaStream_t>(stream));
+    return launch(ev, d_packed, n, d_h, d_logits, static_cast<cudaStream_t>(stream), chan_err(ev, kChanDevice));
 }
 
 int bida_gpu_stream_status(bida_gpu_evaluator *ev) {
     if (!ev)
         return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL evaluator");
-    return collect_errors(ev);
+    return collect_errors(ev, kChanDevice);
 }
 
 int bida_gpu_info(const bida_gpu_evaluator *ev, bida_gpu_model_info *out) {
@@ -677,6 +818,35 @@ int bida_gpu_info(const bida_gpu_evaluator *ev, bida_gpu_model_info *out) {
     out->weights_in_smem = ev->w_in_smem;
     return BIDA_OK;
 }
+
+} // extern "C"
+
+namespace {
+// Installs a device table (ownership passes to the handle); the caller holds
+// every lock of the handle.
+void install_pdb(bida_gpu_evaluator *ev, const uint8_t *pattern, int pattern_len, uint8_t *d, uint64_t n_entries,
+                 int mode) {
+    const int n = ev->domain == BIDA_DOMAIN_RC ? 8 : ev->domain * ev->domain;
+    PdbArgs a{};
+    a.n = n_entries;
+    a.m = pattern_len;
+    a.mode = mode;
+    for (int i = 0; i < pattern_len; ++i) {
+        a.pat[i] = pattern[i];
+        unsigned long long w = 1;  // partial_perm_rank weight (ranking.hpp:43-45)
+        for (int k = 0; k < pattern_len - i - 1; ++k)
+            w *= static_cast<unsigned long long>(n - i - 1 - k);
+        a.w[i] = w;
+    }
+    if (ev->d_pdb)
+        cudaFree(ev->d_pdb);
+    ev->d_pdb = d;
+    a.entries = d;
+    ev->pdb = a;
+}
+} // namespace
+
+extern "C" {
 
 int bida_gpu_attach_pdb(bida_gpu_evaluator *ev, const uint8_t *pattern, int pattern_len,
                         const uint8_t *entries, uint64_t n_entries, int mode) {
@@ -716,17 +886,6 @@ int bida_gpu_attach_pdb(bida_gpu_evaluator *ev, const uint8_t *pattern, int patt
             expect *= 3;
     if (n_entries != expect)
         return fail(BIDA_ERR_RUNTIME, "PDB entry count does not match pattern");
-    PdbArgs a{};
-    a.n = n_entries;
-    a.m = pattern_len;
-    a.mode = mode;
-    for (int i = 0; i < pattern_len; ++i) {
-        a.pat[i] = pattern[i];
-        unsigned long long w = 1;  // partial_perm_rank weight (ranking.hpp:43-45)
-        for (int k = 0; k < pattern_len - i - 1; ++k)
-            w *= static_cast<unsigned long long>(n - i - 1 - k);
-        a.w[i] = w;
-    }
     uint8_t *d = nullptr;
     CUDA_TRY(cudaMalloc(&d, n_entries));
     const cudaError_t e = cudaMemcpy(d, entries, n_entries, cudaMemcpyHostToDevice);
@@ -734,11 +893,24 @@ int bida_gpu_attach_pdb(bida_gpu_evaluator *ev, const uint8_t *pattern, int patt
         cudaFree(d);
         return fail(BIDA_ERR_CUDA, std::string("PDB upload: ") + cudaGetErrorString(e));
     }
-    if (ev->d_pdb)
-        cudaFree(ev->d_pdb);
-    ev->d_pdb = d;
-    a.entries = d;
-    ev->pdb = a;
+    install_pdb(ev, pattern, pattern_len, d, n_entries, mode);
+    return BIDA_OK;
+}
+
+int bida_gpu_attach_pdb_built(bida_gpu_evaluator *ev, const uint8_t *pattern, int pattern_len, int mode) {
+    if (!ev)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL evaluator");
+    if (mode != BIDA_PDB_MIN && mode != BIDA_PDB_REPLACE)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "unknown PDB mode");
+    CUDA_TRY(cudaSetDevice(ev->device));
+    uint8_t *d = nullptr;
+    uint64_t n = 0;
+    if (int rc = bida_gpu::pdb_build_device(ev->domain, pattern, pattern_len, &d, &n))
+        return rc;
+    std::lock_guard<std::mutex> lk(ev->mu);
+    static_assert(kZcLanes == 4, "lock every zero-copy lane");
+    std::scoped_lock lanes(ev->zc[0].mu, ev->zc[1].mu, ev->zc[2].mu, ev->zc[3].mu);
+    install_pdb(ev, pattern, pattern_len, d, n, mode);
     return BIDA_OK;
 }
 
@@ -781,6 +953,16 @@ int bida_gpu_debug_trace(bida_gpu_evaluator *ev, long long *dev_buf) {
 }
 
 int bida_gpu_trace_slots(void) { return mlp_trace_slots(); }
+
+int bida_gpu_exact_replays(bida_gpu_evaluator *ev, int64_t *out) {
+    if (!ev || !out)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL argument");
+    CUDA_TRY(cudaSetDevice(ev->device));
+    unsigned long long v = 0;
+    CUDA_TRY(cudaMemcpy(&v, ev->d_replays, sizeof(v), cudaMemcpyDeviceToHost));
+    *out = static_cast<int64_t>(v);
+    return BIDA_OK;
+}
 
 int64_t bida_gpu_launch_count(const bida_gpu_evaluator *ev) {
     return ev ? ev->launches.load(std::memory_order_relaxed) : 0;

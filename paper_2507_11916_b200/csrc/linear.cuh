@@ -37,6 +37,7 @@ struct LinearArgs {
     int w_in_smem;           // Wt copied to shared memory by every CTA
     int any_rowflag;
     int *err;                // mapped host error words
+    unsigned long long *replays;  // readouts that took the exact float64 replay
     PdbArgs pdb;             // optional PDB correction (pdb.cuh)
 };
 
@@ -133,7 +134,7 @@ linear_eval_kernel(const LinearArgs a) {
                         if (a.logits_out && c < C)
                             a.logits_out[((base + k) * E + m) * C + c] = dot;
                     }
-                    const int h = warp_quantile_certified<CS>(lg, C, a.thr, a.uLo, a.uHi, scratch, lane, a.err);
+                    const int h = warp_quantile_certified<CS>(lg, C, a.thr, a.uLo, a.uHi, scratch, lane, a.err, a.replays);
                     hmin = min(hmin, h);
                 }
             }

@@ -26,7 +26,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -80,6 +82,7 @@ struct MlpParams {
     int32_t *h_out;
     double *logits_out;
     int *err;
+    unsigned long long *replays;  // optional: readouts that took the exact float64 replay
     long long *trace;   // optional debug timeline (CTA 0): [warp][kTraceSlots] (clock64, tag)
     PdbArgs pdb;        // optional PDB correction (pdb.cuh)
     uint8_t *scratch;   // wide: per-CTA hidden activations, 2 buffers of sbytes (global, L2-resident)
@@ -90,6 +93,12 @@ struct MlpParams {
 
 constexpr int kTraceSlots = 256;
 
+// Wide schedule: activation scratch buffers allocated once per model; a launch
+// takes one round-robin and orders itself after the buffer's previous user
+// with an event (stream-ordered reuse, so concurrent callers on different
+// streams never share a buffer in flight).
+constexpr int kScratchPool = 4;
+
 struct MlpModel {
     MlpParams p;
     uint8_t *d_wimg = nullptr;
@@ -98,6 +107,12 @@ struct MlpModel {
     int grid_cap = 148;
     int cm = 32;
     long long *trace = nullptr;  // debug timeline buffer (bida_gpu_debug_trace)
+    std::once_flag attr_once;    // dynamic-smem attribute set at the first launch only
+    cudaError_t attr_err = cudaSuccess;
+    uint8_t *scratch[kScratchPool] = {};
+    cudaEvent_t scratch_ev[kScratchPool] = {};
+    std::mutex scratch_mu[kScratchPool];
+    std::atomic<unsigned> scratch_next{0};
 };
 
 void mlp_set_trace(MlpModel *m, long long *dev_buf) { m->trace = dev_buf; }
@@ -619,6 +634,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                             bool fb = false;
                             const int h =
                                 readout_certified<CM>(v, p.C, p.scale_f[e], p.scale_d[e], p.rk, &dist_bad, &fb);
+                            if (fb && p.replays)
+                                atomicAdd(p.replays, 1ull);
                             hmin = min(hmin, h);
                             tr(fb ? 83 : 82);
                             tr(80);
@@ -1043,6 +1060,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
                         }
                         bool fb = false;
                         const int h = readout_certified<CM>(v, p.C, p.scale_f[e], p.scale_d[e], p.rk, &dist_bad, &fb);
+                        if (fb && p.replays)
+                            atomicAdd(p.replays, 1ull);
                         hmin = min(hmin, h);
                         tr(80);
                     }
@@ -1103,8 +1122,11 @@ int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
     auto kern = p.mode != kWide ? mlp_fused_kernel<DOMAIN, CM>
                 : (p.cluster == 2 ? mlp_wide_kernel<DOMAIN, CM, true> : mlp_wide_kernel<DOMAIN, CM, false>);
     const int threads = kMlpThreads;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(m->smem));
+    std::call_once(m->attr_once, [&] {
+        m->attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(m->smem));
+    });
+    cudaError_t e = m->attr_err;
     if (e != cudaSuccess) {
         g_err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
         return 1;
@@ -1114,8 +1136,13 @@ int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
     if (p.cluster == 2)
         grid = (grid + 1) & ~1;
     MlpParams q = p;
-    if (p.mode == kWide) {  // per-launch scratch from the stream-ordered pool (concurrent launches are safe)
-        e = cudaMallocAsync(reinterpret_cast<void **>(&q.scratch), static_cast<size_t>(grid) * 2 * p.sbytes, st);
+    std::unique_lock<std::mutex> slk;
+    int sslot = -1;
+    if (p.mode == kWide) {
+        sslot = static_cast<int>(m->scratch_next.fetch_add(1, std::memory_order_relaxed) % kScratchPool);
+        slk = std::unique_lock<std::mutex>(m->scratch_mu[sslot]);
+        q.scratch = m->scratch[sslot];
+        e = cudaStreamWaitEvent(st, m->scratch_ev[sslot], 0);
         if (e != cudaSuccess) {
             g_err = std::string("mlp scratch: ") + cudaGetErrorString(e);
             return 1;
@@ -1140,8 +1167,8 @@ int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
     }
     if (e == cudaSuccess)
         e = cudaGetLastError();
-    if (p.mode == kWide) {
-        const cudaError_t fe = cudaFreeAsync(q.scratch, st);
+    if (sslot >= 0) {
+        const cudaError_t fe = cudaEventRecord(m->scratch_ev[sslot], st);
         if (e == cudaSuccess)
             e = fe;
     }
@@ -1439,13 +1466,15 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
         return fail(err, 3, std::string("BMLP1 upload: ") + cudaGetErrorString(ce));
     }
     if (p.mode == kWide) {
-        // scratch comes from the device's stream-ordered pool per launch: keep
-        // freed blocks in the pool instead of returning them at every sync
-        int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t keep = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        const size_t sb = static_cast<size_t>(((m->grid_cap + 1) & ~1)) * 2 * static_cast<size_t>(p.sbytes);
+        for (int i = 0; i < kScratchPool && ce == cudaSuccess; ++i) {
+            ce = cudaMalloc(reinterpret_cast<void **>(&m->scratch[i]), sb);
+            if (ce == cudaSuccess)
+                ce = cudaEventCreateWithFlags(&m->scratch_ev[i], cudaEventDisableTiming);
+        }
+        if (ce != cudaSuccess) {
+            mlp_destroy(m);
+            return fail(err, 3, std::string("BMLP1 scratch: ") + cudaGetErrorString(ce));
         }
     }
     p.wimg = m->d_wimg;
@@ -1461,7 +1490,8 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
 }
 
 int mlp_launch(MlpModel *m, int domain, const void *d_packed, int64_t n, int32_t *d_h, double *d_logits,
-               int *err_dev, cudaStream_t st, std::atomic<int64_t> *launches, const PdbArgs *pdb) {
+               int *err_dev, unsigned long long *replays, cudaStream_t st, std::atomic<int64_t> *launches,
+               const PdbArgs *pdb) {
     MlpParams p = m->p;  // per-call copy: concurrent launches on one handle are safe
     if (pdb)
         p.pdb = *pdb;
@@ -1473,6 +1503,7 @@ int mlp_launch(MlpModel *m, int domain, const void *d_packed, int64_t n, int32_t
     p.h_out = d_h;
     p.logits_out = d_logits;
     p.err = err_dev;
+    p.replays = replays;
     int rc;
     switch (domain) {
     case kSTP2: rc = launch_d<kSTP2>(m, p, st); break;
@@ -1492,6 +1523,12 @@ void mlp_destroy(MlpModel *m) {
         cudaFree(m->d_wimg);
     if (m->d_bias)
         cudaFree(m->d_bias);
+    for (int i = 0; i < kScratchPool; ++i) {
+        if (m->scratch[i])
+            cudaFree(m->scratch[i]);
+        if (m->scratch_ev[i])
+            cudaEventDestroy(m->scratch_ev[i]);
+    }
     delete m;
 }
 

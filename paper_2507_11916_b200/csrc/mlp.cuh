@@ -24,8 +24,8 @@ int mlp_create(const unsigned char *blob, size_t len, int F, double thr, int num
 // Enqueues the fused encode + MLP + readout on `st`; returns 0 or nonzero
 // (message in mlp_last_error()).
 int mlp_launch(MlpModel *m, int domain, const void *d_packed, int64_t n, int32_t *d_h,
-               double *d_logits, int *err_dev, cudaStream_t st, std::atomic<int64_t> *launches,
-               const PdbArgs *pdb = nullptr);
+               double *d_logits, int *err_dev, unsigned long long *replays, cudaStream_t st,
+               std::atomic<int64_t> *launches, const PdbArgs *pdb = nullptr);
 void mlp_destroy(MlpModel *m);
 // Debug: record a per-warp clock64 timeline of CTA 0 into dev_buf ([10 warps][mlp_trace_slots()]).
 void mlp_set_trace(MlpModel *m, long long *dev_buf);

@@ -129,7 +129,8 @@ namespace bida_gpu {
 // are excluded from the relative bound.  Undecided -> exact sequential replay.
 template <int CS>
 __device__ __forceinline__ int warp_quantile_certified(double (&lg)[CS], int C, double thr, float uLo,
-                                                       float uHi, double *scratch, int lane, int *err_bits) {
+                                                       float uHi, double *scratch, int lane, int *err_bits,
+                                                       unsigned long long *replays = nullptr) {
     bool finite = true;
     double mx = -INFINITY;
 #pragma unroll
@@ -201,6 +202,8 @@ __device__ __forceinline__ int warp_quantile_certified(double (&lg)[CS], int C, 
         if (!ambiguous)
             return above;  // smallest k with T_k <= A (T_k non-increasing in k)
     }
+    if (replays && lane == 0)
+        atomicAdd(replays, 1ull);
     return warp_quantile_exact<CS>(lg, C, thr, scratch, lane, err_bits);
 }
 

@@ -141,6 +141,7 @@ class RefLib:
         L.ref_pdb_lookup_file.argtypes = [C.c_int, C.c_char_p, _p, _i64, _p]
         L.ref_pdb_build_save.argtypes = [C.c_int, _p, C.c_int, C.c_char_p]
         L.ref_load_instances.argtypes = [C.c_int, C.c_char_p, _p, _i64, C.POINTER(_i64)]
+        L.ref_readout_scaled_logits.argtypes = [C.c_int, _p, _p, C.c_int, C.c_int, C.c_double, _i64, _p, C.c_int]
         self.L = L
 
     def _check(self, rc):
@@ -214,6 +215,17 @@ class RefLib:
         out = np.zeros(len(packed), np.int32)
         self._check(self.L.ref_pdb_lookup_file(domain, path.encode(), _ptr(packed), len(packed), _ptr(out)))
         return out
+
+    def readout_scaled_logits(self, domain, acc, scale, q, threads=1):
+        """The reference's LinearModelBackend::evaluate readout (softmax,
+        quantile_class, ensemble_min) on logits (double)acc * (double)scale;
+        acc int32 [n][E][C], scale float32 [E] (ref_harness.cpp)."""
+        acc = np.ascontiguousarray(acc, np.int32)
+        scale = np.ascontiguousarray(scale, np.float32)
+        n, E, Cc = acc.shape
+        h = np.zeros(n, np.int32)
+        self._check(self.L.ref_readout_scaled_logits(domain, _ptr(acc), _ptr(scale), E, Cc, q, n, _ptr(h), threads))
+        return h
 
     def load_instances(self, domain, path, cap=100000):
         out = np.zeros(cap, packed_dtype(domain))
