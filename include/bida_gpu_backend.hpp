@@ -73,7 +73,11 @@ inline void throw_status(int rc, const char *what) {
 }
 
 template <class D>
-class GpuBackend final : public bida::EvaluatorBackend<D> {
+class GpuBackend final : public bida::EvaluatorBackend<D>
+#ifdef BIDA_RING_EVALUATOR
+    , public bida::ConcurrentBackend  // the C-ABI handle is re-entrant (4 zero-copy lanes)
+#endif
+{
 public:
     using Traits = DomainOf<D>;
 
@@ -132,6 +136,9 @@ public:
     GpuBackend &operator=(const GpuBackend &) = delete;
 
     bool needs_features() const override { return false; }
+#ifdef BIDA_RING_EVALUATOR
+    int max_concurrent_calls() const override { return 4; }  // zero-copy lanes per handle (bida_gpu.cu)
+#endif
 
     void evaluate(std::span<const bida::BatchItem<D>> batch, std::span<std::int32_t> out) override {
         thread_local std::vector<unsigned char> staging;

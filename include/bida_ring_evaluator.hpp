@@ -54,6 +54,13 @@
 
 namespace bida {
 
+// Opt-in marker for backends whose evaluate() may run on several agent threads
+// at once (the reference's EvaluatorBackend interface is unchanged).
+struct ConcurrentBackend {
+    virtual ~ConcurrentBackend() = default;
+    virtual int max_concurrent_calls() const = 0;
+};
+
 namespace ring_detail {
 inline std::int64_t now_ns() {
     return std::chrono::duration_cast<std::chrono::nanoseconds>(
@@ -64,6 +71,15 @@ inline int default_agents() {
     const char *s = std::getenv("BIDA_EVAL_AGENTS");
     const int k = s ? std::atoi(s) : 2;
     return std::clamp(k, 1, 16);
+}
+// K concurrent agents only for backends that declare concurrent evaluate()
+// calls safe and useful (ConcurrentBackend, e.g. bida_gpu::GpuBackend); any
+// other backend (TableSimBackend, LinearModelBackend) keeps the reference's
+// one agent per evaluator, i.e. one simulated device per evaluator.
+template <class B>
+int agents_for(const B *backend, int requested) {
+    const auto *c = dynamic_cast<const ConcurrentBackend *>(backend);
+    return c ? std::clamp(requested, 1, std::max(1, c->max_concurrent_calls())) : 1;
 }
 inline int default_shards() {
     const char *s = std::getenv("BIDA_EVAL_SHARDS");
@@ -97,8 +113,10 @@ public:
         if (capacity_ == 0)
             throw std::invalid_argument("Evaluator: capacity must be >= 1");
         nshards_ = static_cast<std::size_t>(shards);
+        // every shard holds at least one full batch, so a producer blocked on
+        // a full shard always leaves a flushable batch behind it (timeout < 0)
         std::size_t r = 4096;
-        while (r * nshards_ < 8 * capacity_)
+        while (r < capacity_ || r * nshards_ < 8 * capacity_)
             r <<= 1;
         ring_size_ = r;
         mask_ = r - 1;
@@ -113,9 +131,11 @@ public:
         // a producer wakes the agents when its shard goes nonempty or crosses
         // a multiple of capacity / shards (the agents then check the total)
         wake_step_ = std::max<std::uint64_t>(1, capacity_ / nshards_);
-        if (!immediate_)
-            for (int k = 0; k < agents; ++k)
+        if (!immediate_) {
+            const int k_agents = ring_detail::agents_for(backend_.get(), agents);
+            for (int k = 0; k < k_agents; ++k)
                 agents_.emplace_back([this] { agent_loop(); });
+        }
     }
 
     ~Evaluator() { close(); }
@@ -133,30 +153,23 @@ public:
             immediate_submitted_.fetch_add(1, std::memory_order_relaxed);
             return t;
         }
-        // A submit that races close() itself (not a pattern the search uses:
-        // groups close after their searchers join) may land after the agents
-        // drained; the reference closes that window with its buffer mutex.
-        if (closed_.load(std::memory_order_acquire))
-            throw std::runtime_error("Evaluator: submission after shutdown");
-        // each searcher thread stays on one shard: the tail it bumps is
-        // shared with ~threads/shards others instead of with every thread
-        Shard &sh = shards_[ring_detail::thread_slot() % nshards_];
-        const std::uint64_t pos = sh.tail.fetch_add(1, std::memory_order_acq_rel);
-        Meta &m = sh.meta[pos & mask_];
-        unsigned spins = 0;
-        while (m.seq.load(std::memory_order_acquire) != pos) // shard full: wait for the lap to drain
-            ring_detail::relax(spins);
-        BatchItem<D> &it = sh.items[pos & mask_];
-        it.ticket = t;
-        it.state = state;
-        it.features = std::move(features);
-        if (timeout_us_ > 0)
-            m.t_ns = ring_detail::now_ns();
-        m.seq.store(pos + 1, std::memory_order_seq_cst);
-        const std::uint64_t depth = pos + 1 - sh.head.load(std::memory_order_seq_cst);
-        if (depth == 1 || (depth <= ring_size_ && depth % wake_step_ == 0))
-            wake();
+        enqueue(state, std::move(features), t, nullptr);
         return t;
+    }
+
+    // Extension for the CB-DFS overlay (include/overlay/bida/cbdfs.hpp): the
+    // caller owns `slot` (value -1, address stable until it is resolved), so
+    // no per-node shared_ptr is allocated.  Same batching as submit().
+    void submit_slot(const typename D::State &state, FeatureVector features, TicketSlot *slot) {
+        if (immediate_) {
+            BatchItem<D> item{Ticket(), state, std::move(features)};
+            std::int32_t v = 0;
+            backend_->evaluate(std::span<const BatchItem<D>>(&item, 1), std::span<std::int32_t>(&v, 1));
+            resolve(*slot, v);
+            immediate_submitted_.fetch_add(1, std::memory_order_relaxed);
+            return;
+        }
+        enqueue(state, std::move(features), Ticket(), slot);
     }
 
     bool needs_features() const { return backend_->needs_features(); }
@@ -200,8 +213,15 @@ public:
 
     // Drains everything submitted (resolving it) and joins the agents.
     void close() {
-        if (closed_.exchange(true, std::memory_order_acq_rel))
+        if (closed_.exchange(true, std::memory_order_seq_cst))
             return;
+        for (std::size_t k = 0; k < nshards_; ++k) {
+            unsigned spins = 0;
+            while (shards_[k].inflight.load(std::memory_order_seq_cst) != 0)
+                ring_detail::relax(spins);
+        }
+        // every accepted submit is now published: agents may exit once drained
+        quiesced_.store(true, std::memory_order_seq_cst);
         wake();
         for (auto &a : agents_)
             if (a.joinable())
@@ -228,9 +248,11 @@ private:
     struct Meta {
         std::atomic<std::uint64_t> seq{0}; // == pos: free for lap pos; == pos+1: published
         std::int64_t t_ns = 0;             // submit time (timeout > 0 only)
+        TicketSlot *raw = nullptr;         // submit_slot(): resolve here instead of the item's ticket
     };
     struct Shard {
         alignas(64) std::atomic<std::uint64_t> tail{0}; // next position producers claim
+        std::atomic<std::uint32_t> inflight{0};         // submits between the closed check and publish
         alignas(64) std::atomic<std::uint64_t> head{0}; // next position agents claim
         std::unique_ptr<BatchItem<D>[]> items;
         std::unique_ptr<Meta[]> meta;
@@ -240,6 +262,36 @@ private:
         std::uint64_t h;
         std::size_t n;
     };
+
+    void enqueue(const typename D::State &state, FeatureVector features, Ticket t, TicketSlot *raw) {
+        // each searcher thread stays on one shard: the tail it bumps is
+        // shared with ~threads/shards others instead of with every thread
+        Shard &sh = shards_[ring_detail::thread_slot() % nshards_];
+        // close() waits for in-flight submits (Dekker pairing with closed_), so
+        // a submit that passed the check is always drained before the agents exit
+        sh.inflight.fetch_add(1, std::memory_order_seq_cst);
+        if (closed_.load(std::memory_order_seq_cst)) {
+            sh.inflight.fetch_sub(1, std::memory_order_release);
+            throw std::runtime_error("Evaluator: submission after shutdown");
+        }
+        const std::uint64_t pos = sh.tail.fetch_add(1, std::memory_order_acq_rel);
+        Meta &m = sh.meta[pos & mask_];
+        unsigned spins = 0;
+        while (m.seq.load(std::memory_order_acquire) != pos) // shard full: wait for the lap to drain
+            ring_detail::relax(spins);
+        BatchItem<D> &it = sh.items[pos & mask_];
+        it.ticket = std::move(t);
+        it.state = state;
+        it.features = std::move(features);
+        m.raw = raw;
+        if (timeout_us_ > 0)
+            m.t_ns = ring_detail::now_ns();
+        m.seq.store(pos + 1, std::memory_order_seq_cst);
+        sh.inflight.fetch_sub(1, std::memory_order_release);
+        const std::uint64_t depth = pos + 1 - sh.head.load(std::memory_order_seq_cst);
+        if (depth == 1 || (depth <= ring_size_ && depth % wake_step_ == 0))
+            wake();
+    }
 
     bool pending() const {
         for (std::size_t k = 0; k < nshards_; ++k)
@@ -273,6 +325,8 @@ private:
         std::size_t rot = 0;
         for (;;) {
             const std::uint32_t e = epoch_.load(std::memory_order_seq_cst);
+            // read before the scan: once set, nothing new can be published
+            const bool quiesced = quiesced_.load(std::memory_order_seq_cst);
             std::unique_lock<std::mutex> lk(claim_m_);
             // published work per shard, starting from a rotating shard so no
             // shard starves when the total exceeds one batch
@@ -297,7 +351,7 @@ private:
             const bool closed = closed_.load(std::memory_order_acquire);
             if (n == 0) {
                 lk.unlock();
-                if (closed && drained)
+                if (quiesced && drained)
                     return;
                 if (closed || !drained) { // a producer is mid-publish
                     std::this_thread::yield();
@@ -315,6 +369,12 @@ private:
                     due = true;
                 } else {
                     lk.unlock();
+                    // one agent watches the deadline; the others park on the
+                    // epoch (producers wake them) instead of spinning too
+                    if (deadline_owner_.exchange(true, std::memory_order_acq_rel)) {
+                        epoch_.wait(e, std::memory_order_seq_cst);
+                        continue;
+                    }
                     // sleep_for rounds up to the timer slack (~50 us): below
                     // that, re-check between yields so a filling batch or a
                     // short deadline is seen on time
@@ -322,6 +382,7 @@ private:
                         std::this_thread::yield();
                     else
                         std::this_thread::sleep_for(std::chrono::microseconds(100));
+                    deadline_owner_.store(false, std::memory_order_release);
                     continue;
                 }
             } else if (!due) {
@@ -366,7 +427,9 @@ private:
             Shard &sh = shards_[r.shard];
             for (std::size_t i = 0; i < r.n; ++i, ++o) {
                 BatchItem<D> &it = in_place ? sh.items[(r.h + i) & mask_] : scratch[o];
-                resolve(*it.ticket, vals[o]);
+                Meta &mt = sh.meta[(r.h + i) & mask_];
+                resolve(mt.raw ? *mt.raw : *it.ticket, vals[o]);
+                mt.raw = nullptr;
                 it.ticket.reset();
                 if (!it.features.empty())
                     FeatureVector().swap(it.features);
@@ -394,6 +457,8 @@ private:
     alignas(64) std::atomic<std::uint32_t> epoch_{0};
     std::atomic<bool> force_{false};
     std::atomic<bool> closed_{false};
+    std::atomic<bool> deadline_owner_{false};
+    std::atomic<bool> quiesced_{false};  // close(): closed_ set and no submit in flight
     std::mutex claim_m_;
     std::vector<std::thread> agents_;
 
@@ -434,6 +499,19 @@ public:
         }
         return e.submit(state, std::move(x));
     }
+
+    // Extension (CB-DFS overlay): submit_state with a caller-owned ticket slot.
+    void submit_state_slot(int thread_id, const typename D::State &state, TicketSlot *slot) {
+        Evaluator<D> &e = of(thread_id);
+        FeatureVector x;
+        if (e.needs_features()) {
+            x.resize(static_cast<std::size_t>(D::feature_length()));
+            D::encode(state, x.data());
+        }
+        e.submit_slot(state, std::move(x), slot);
+    }
+
+    bool needs_features() const { return evs_.front()->needs_features(); }
 
     int evaluate_single(const typename D::State &state) {
         FeatureVector x(static_cast<std::size_t>(D::feature_length()));

@@ -63,6 +63,7 @@ int main() {
         wait_all(ts, 2);
         for (int i = 0; i < 8; ++i)
             CHECK(poll(ts[i]) == mh.lookup(ss[i]));
+        ev.close();  // tickets resolve before record_batch runs (batch_eval.hpp:350-352): join first
         const SearchStats st = ev.stats_snapshot();
         CHECK(st.batches == 1 && st.batch_items == 8 && st.max_batch_occupancy == 8);
     }
@@ -71,6 +72,7 @@ int main() {
         const Ticket t = ev.submit(D::solved(), {});
         wait_all({t}, 2);
         CHECK(poll(t) == 0);
+        ev.close();
         CHECK(ev.stats_snapshot().batches == 1);
     }
     { // no submissions, no flushes
@@ -86,6 +88,7 @@ int main() {
         for (std::size_t i = 0; i < 10 * B; ++i)
             ts.push_back(ev.submit(walk(rng), {}));
         wait_all(ts, 5);
+        ev.close();
         const SearchStats st = ev.stats_snapshot();
         CHECK(st.batches == 10 && st.batch_items == 10 * B && st.max_batch_occupancy == B);
     }
@@ -112,6 +115,7 @@ int main() {
         ev.request_flush();
         wait_all({t}, 2);
         CHECK(poll(t) == 0);
+        ev.close();
         CHECK(ev.stats_snapshot().forced_flushes == 1);
     }
     { // group: evaluate_single, even routing
@@ -179,6 +183,63 @@ int main() {
         CHECK(ev.stats_snapshot().batch_items == n);
     }
 #ifdef BIDA_RING_EVALUATOR
+    { // ring only: more shards than 8 with a large batch and no timeout:
+      // every shard holds a full batch, so a lone producer never stalls
+        Evaluator<D> ev(sim(), 16384, -1, false, 1, 16);
+        std::mt19937_64 rng(11);
+        std::vector<Ticket> ts;
+        for (int i = 0; i < 40000; ++i)
+            ts.push_back(ev.submit(walk(rng, 5), {}));
+        ev.request_flush();
+        wait_all(ts, 10);
+        ev.close();
+        for (const auto &t : ts)
+            CHECK(poll(t) >= 0);
+        CHECK(ev.stats_snapshot().batches == 3);
+    }
+    { // ring only: caller-owned ticket slots (submit_slot), resolved in place
+        Evaluator<D> ev(sim(), 32, 0, false, 2, 4);
+        std::mt19937_64 rng(12);
+        std::vector<TicketSlot> slots(5000);
+        std::vector<D::State> ss;
+        for (auto &sl : slots) {
+            ss.push_back(walk(rng, 7));
+            ev.submit_slot(ss.back(), {}, &sl);
+        }
+        ev.close();
+        for (std::size_t i = 0; i < slots.size(); ++i)
+            CHECK(slots[i].value.load() == mh.lookup(ss[i]));
+        CHECK(ev.resolved() == slots.size() && ev.double_resolutions() == 0);
+    }
+    { // ring only: submits racing close(): every accepted submit is resolved,
+      // every other one throws; nothing hangs
+        for (int round = 0; round < 50; ++round) {
+            Evaluator<D> ev(sim(), 8, -1, false, 2, 4);
+            std::atomic<bool> go{true};
+            std::vector<std::thread> th;
+            std::vector<std::vector<Ticket>> got(4);
+            for (int k = 0; k < 4; ++k)
+                th.emplace_back([&, k] {
+                    std::mt19937_64 rng(1000 * round + k);
+                    while (go.load()) {
+                        try {
+                            got[k].push_back(ev.submit(walk(rng, 4), {}));
+                        } catch (const std::runtime_error &) {
+                            return;
+                        }
+                    }
+                });
+            std::this_thread::sleep_for(std::chrono::microseconds(200 + 37 * round));
+            ev.close();
+            go.store(false);
+            for (auto &t : th)
+                t.join();
+            for (auto &v : got)
+                for (auto &t : v)
+                    CHECK(poll(t) >= 0);
+            CHECK(ev.submitted() == ev.resolved());
+        }
+    }
     std::printf("ring evaluator: %s\n", failures ? "FAILED" : "all checks passed");
 #else
     std::printf("reference evaluator: %s\n", failures ? "FAILED" : "all checks passed");

@@ -202,6 +202,11 @@ constexpr const char *kEvaluatorImpl = "ring"; // include/bida_ring_evaluator.hp
 #else
 constexpr const char *kEvaluatorImpl = "reference"; // batch_eval.hpp:193-473
 #endif
+#ifdef BIDA_FAST_CBDFS
+constexpr const char *kSearchImpl = "fast"; // include/bida_fast_cbdfs.hpp
+#else
+constexpr const char *kSearchImpl = "reference"; // cbdfs.hpp:254-415
+#endif
 
 const char *status_name(SearchStatus s) {
     switch (s) {
@@ -256,16 +261,15 @@ int run(const Args &a) {
             js << "], \"threads\": " << a.threads << ", \"work_num\": " << a.work_num << ", \"batch\": " << a.batch
                << ", \"timeout_us\": " << a.timeout_us << ", \"evaluators\": " << a.evaluators
                << ", \"evaluator_impl\": \"" << kEvaluatorImpl << "\""
+               << ", \"search_impl\": \"" << kSearchImpl << "\"" << ", \"solution\": [";
+            for (std::size_t k = 0; k < r.solution.size(); ++k)
+                js << (k ? ", " : "") << static_cast<int>(r.solution[k]);
+            js << "]"
                << ", \"immediate\": " << (a.immediate ? "true" : "false")
                << ", \"table1_corners\": " << a.table1_corners << ", \"gpu_pdb\": " << (a.gpu_pdb ? "true" : "false")
                << ", \"algo\": \"" << a.algo << "\"}";
             std::printf("%s\n", js.str().c_str());
             std::fflush(stdout);
-        }
-        if (mode == "gpu") {
-            for (std::size_t e = 0; e < group.evaluator_count(); ++e) {
-                (void)e;
-            }
         }
         group.close();
     }
