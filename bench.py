@@ -43,6 +43,7 @@ WORKLOADS = {
     "rc-mlp-h1610": dict(domain="rc", kind="mlp", H=[1610, 1610], E=1, C=21, q=0.5, batch=1 << 21),
 }
 DEFAULT_WORKLOAD = "rc-mlp-h128"
+LINEAR_WORKLOAD = "rc-linear-e1-c21"
 WIDE_WORKLOAD = "rc-mlp-h1610"
 
 PACKED = {"rc": 16, "stp4": 8, "stp3": 8, "stp2": 8}
@@ -235,7 +236,7 @@ def run_ours(args, wl, rank, world, local, e2e=True):
         clk.__exit__(None, None, None)
         be.close()
         return dict(B=B, nbuf=nbuf, total_ms=total_ms_max, kern_avg_ms=kern_avg_ms, launches=launches,
-                    clocks=clk.summary())
+                    clocks=clk.summary(), host0=host[0])
 
     # ---- end-to-end through the C-ABI with host buffers (e2e) ------------
     try:
@@ -259,7 +260,7 @@ def run_ours(args, wl, rank, world, local, e2e=True):
     clocks = clk.summary()
     be.close()
     return dict(B=B, nbuf=nbuf, total_ms=total_ms_max, kern_avg_ms=kern_avg_ms, launches=launches,
-                e2e_s=e2e_s_max, clocks=clocks)
+                e2e_s=e2e_s_max, clocks=clocks, host0=host[0])
 
 
 # --------------------------------------------------------- CPU baselines
@@ -301,7 +302,10 @@ def cpu_eval_fn(wl, packed, threads):
     return run, "port"
 
 
-def cpu_rate(wl, seconds_target, threads, seed=7):
+def cpu_rate(wl, seconds_target, threads, seed=7, source=None):
+    """Returns (run, kind, states, sample): run() evaluates `sample` (reps
+    times) on the CPU.  `source`: draw the sample from these packed states
+    (the timed batch) instead of fresh random walks."""
     import paper_2507_11916_b200 as bida
 
     # calibrate on a small sample, then size the sample to ~seconds_target
@@ -317,7 +321,11 @@ def cpu_rate(wl, seconds_target, threads, seed=7):
     # RC), so the sample is capped at 2^19 states and repeated to fill the time
     n = int(max(probe_n, min(1 << 19, want)))
     reps = int(max(1, round(want / n)))
-    packed = bida.random_walks(wl["domain"], n, 0, 30, seed=seed + 1)
+    if source is not None:
+        n = min(n, len(source))
+        packed = np.ascontiguousarray(source[:n])
+    else:
+        packed = bida.random_walks(wl["domain"], n, 0, 30, seed=seed + 1)
     run1, kind = cpu_eval_fn(wl, packed, threads)
 
     def run():
@@ -325,7 +333,7 @@ def cpu_rate(wl, seconds_target, threads, seed=7):
             out = run1()
         return out
 
-    return run, kind, n * reps
+    return run, kind, n * reps, packed
 
 
 SEARCH_WALKS = "1:15:15:2508"  # one walk-15 Rubik's scramble (configs[1]: walks 14-16)
@@ -399,7 +407,7 @@ def run_reference_arm(args, wl, rank, world):
     if rank != 0:
         return None
     threads = host_cores()
-    run, kind, n = cpu_rate(wl, args.ref_step_seconds, threads)
+    run, kind, n, _ = cpu_rate(wl, args.ref_step_seconds, threads)
     for _ in range(args.warmup):
         run()
     times = []
@@ -420,6 +428,80 @@ def run_reference_arm(args, wl, rank, world):
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+
+
+def cpu_baseline_and_parity(args, wl, timed_batch, local):
+    """cpu_baseline leg: the reference's CPU evaluator (oracle/_ref) or the
+    oracle port on all host threads over the first states of the timed batch;
+    the same states through the GPU C-ABI give the parity check (flips = h
+    differences, exact_replays = readouts that took the float64 replay)."""
+    threads = host_cores()
+    run, kind, n, sample = cpu_rate(wl, args.cpu_seconds, threads, source=timed_batch)
+    t0 = time.perf_counter()
+    want = run()
+    dt = time.perf_counter() - t0
+    cpu = {"value": n / dt, "unit": "evals/s", "cores": threads, "kind": kind,
+           "sample": f"first {len(sample)} states of the timed batch (packed {wl['domain']} random walks, lengths "
+                     f"0-30) x {n // len(sample)} repetition(s), {dt:.1f} s"}
+    be = make_backend(wl, local)
+    h = be.evaluate(sample)
+    replays = be.exact_replays()
+    be.close()
+    flips = int((np.asarray(h) != np.asarray(want)).sum())
+    parity = {"sample": len(sample), "flips": flips, "exact_replays": replays,
+              "checker": "oracle/_ref LinearModelBackend<D>::evaluate (reference, unchanged)" if kind == "reference"
+              else "oracle/bida_oracle.c BMLP1 port, pinned to torch-float64 + reference-readout goldens",
+              "path": "bida_gpu_evaluate (C-ABI), same states as the cpu_baseline sample"}
+    return cpu, parity
+
+
+def batch_sweep(wl, local, sizes=None):
+    """BASELINE configs[2]: evals/s vs batch size 2^10..2^20 on one GPU, device-
+    resident (CUDA events over R back-to-back launches on the launching
+    stream; small batches are L2-resident by construction -- the latency
+    regime) and end to end through bida_gpu_evaluate from page-locked host
+    buffers (wall clock per synchronous call, what a search agent waits on)."""
+    import torch
+
+    import paper_2507_11916_b200 as bida
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    sizes = sizes or [1 << k for k in range(10, 21)]
+    be = make_backend(wl, local)
+    _, fl = algorithmic(wl)
+    stream = torch.cuda.current_stream()
+    out = []
+    for B in sizes:
+        host = bida.random_walks(wl["domain"], B, 0, 30, seed=B)
+        d_in = torch.from_numpy(host.view(np.uint8).copy()).to(dev)
+        d_h = torch.empty(B, dtype=torch.int32, device=dev)
+        R = int(min(2000, max(20, (1 << 23) // B)))
+        for _ in range(3):
+            be.evaluate_device(d_in, d_h)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(R):
+            be.evaluate_device(d_in, d_h)
+        b.record(stream)
+        torch.cuda.synchronize()
+        be.status()
+        dev_us = a.elapsed_time(b) * 1000.0 / R
+        hp = torch.from_numpy(host.view(np.uint8).copy()).pin_memory().numpy().view(host.dtype)
+        ho = torch.empty(B, dtype=torch.int32).pin_memory().numpy()
+        Re = int(min(1000, max(10, (1 << 22) // B)))
+        for _ in range(3):
+            be.evaluate(hp, out=ho)
+        t0 = time.perf_counter()
+        for _ in range(Re):
+            be.evaluate(hp, out=ho)
+        e2e_us = (time.perf_counter() - t0) * 1e6 / Re
+        out.append({"batch": B, "device_us_per_call": dev_us, "device_evals_per_s": B / dev_us * 1e6,
+                    "e2e_us_per_call": e2e_us, "e2e_evals_per_s": B / e2e_us * 1e6,
+                    "device_tops": fl * B / dev_us / 1e6 if wl["kind"] == "mlp" else None})
+    be.close()
+    return out
 
 
 def roofline_for(name, wl, B, kern_avg_ms):
@@ -466,6 +548,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-wide-leg", dest="wide_leg", action="store_false",
                     help="skip the config-4 (H=1610) device-resident leg of an N=1 run")
+    ap.add_argument("--no-linear-leg", dest="linear_leg", action="store_false",
+                    help="skip the reference-model (rc-linear-e1-c21) leg of an N=1 run")
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false",
+                    help="skip the batch-size sweep (BASELINE configs[2]) of an N=1 run")
     ap.add_argument("--search-seconds", type=float, default=10.0,
                     help="Batch IDA* nodes/s leg (RC MLP workloads, N=1); 0 disables")
     args = ap.parse_args()
@@ -526,15 +612,24 @@ def main():
             "batch_per_gpu": rw["B"], "kernel_ms_avg": rw["kern_avg_ms"], "gpu_launches": int(rw["launches"]),
             "roofline": roofline_for(WIDE_WORKLOAD, ww, rw["B"], rw["kern_avg_ms"]), "clocks": rw["clocks"]}
     if world == 1 and not args.no_cpu_baseline:
-        threads = host_cores()
-        run, kind, n = cpu_rate(wl, args.cpu_seconds, threads)
-        t0 = time.perf_counter()
-        run()
-        dt = time.perf_counter() - t0
-        line["cpu_baseline"] = {
-            "value": n / dt, "unit": "evals/s", "cores": threads, "kind": kind,
-            "sample": f"{n} packed {wl['domain']} random-walk states (lengths 0-30), one call, {dt:.1f} s",
-        }
+        line["cpu_baseline"], line["parity"] = cpu_baseline_and_parity(args, wl, r["host0"], local)
+    if world == 1 and args.linear_leg and wl["kind"] != "linear":
+        # the reference's own model (LinearModelBackend, BLIN1): device value, e2e,
+        # roofline and its reference CPU baseline on the same timed batch
+        lw = WORKLOADS[LINEAR_WORKLOAD]
+        rl = run_ours(args, lw, rank, world, local)
+        leg = {"workload": LINEAR_WORKLOAD, "model": {k: v for k, v in lw.items() if k in ("kind", "E", "C", "q")},
+               "value": whole_job_rate(rl["B"], args.steps, world, rl["total_ms"]), "unit": "evals/s",
+               "batch_per_gpu": rl["B"], "kernel_ms_avg": rl["kern_avg_ms"], "gpu_launches": int(rl["launches"]),
+               "e2e": {"value": rl["B"] * args.steps / rl["e2e_s"], "unit": "evals/s",
+                       "h2d_bytes_per_step": rl["B"] * PACKED[lw["domain"]], "d2h_bytes_per_step": rl["B"] * 4},
+               "roofline": roofline_for(LINEAR_WORKLOAD, lw, rl["B"], rl["kern_avg_ms"]), "clocks": rl["clocks"]}
+        if not args.no_cpu_baseline:
+            leg["cpu_baseline"], leg["parity"] = cpu_baseline_and_parity(args, lw, rl["host0"], local)
+        line["linear_model"] = leg
+    if world == 1 and args.sweep:
+        line["batch_sweep"] = {"workload": args.workload, "config": "BASELINE configs[2]: batch 2^10..2^20",
+                               "points": batch_sweep(wl, local)}
     if world == 1 and args.search_seconds > 0:
         threads = host_cores()
         sr = search_leg(wl, args.search_seconds, threads, cpu=False)

@@ -252,6 +252,12 @@ int orc_bmlp1_parse(const void *blob, size_t len, int F_expected, orc_mlp *m) {
             ly->W = (int8_t *)malloc(nw);
             memcpy(ly->W, b + off, nw);
             off += nw;
+            if (l == 0) {
+                ly->WT = (int8_t *)malloc(nw);
+                for (int o = 0; o < ly->out; ++o)
+                    for (int i = 0; i < ly->in; ++i)
+                        ly->WT[(size_t)i * ly->out + o] = ly->W[(size_t)o * ly->in + i];
+            }
             if (off + 4 * (size_t)ly->out > len) { orc_mlp_free(m); return ORC_ERR_TRUNCATED; }
             ly->bias = (int32_t *)malloc(4 * (size_t)ly->out);
             memcpy(ly->bias, b + off, 4 * (size_t)ly->out);
@@ -278,6 +284,7 @@ void orc_mlp_free(orc_mlp *m) {
     if (m->layers) {
         for (int i = 0; i < m->E * (m->L + 1); ++i) {
             free(m->layers[i].W);
+            free(m->layers[i].WT);
             free(m->layers[i].bias);
         }
     }
@@ -293,32 +300,59 @@ static int mlp_eval_range(const orc_mlp *m, int domain, double q, const void *pa
     for (int l = 0; l < m->L; ++l)
         if (m->H[l] > maxw) maxw = m->H[l];
     if (m->C > maxw) maxw = m->C;
-    int32_t *a = (int32_t *)malloc(sizeof(int32_t) * maxw);
+    uint8_t *a = (uint8_t *)malloc(maxw);  /* hidden activations, 0..255 */
     int32_t *nx = (int32_t *)malloc(sizeof(int32_t) * maxw);
+    int32_t *nx2 = (int32_t *)malloc(sizeof(int32_t) * maxw);
     double *lg = (double *)malloc(sizeof(double) * m->C);
     double *p = (double *)malloc(sizeof(double) * m->C);
     int idx[32];
     int rc = ORC_OK;
     for (int64_t i = lo; i < hi && rc == ORC_OK; ++i) {
-        const int k = orc_active_indices(domain, (const char *)packed + i * pb, idx);
+        int k = orc_active_indices(domain, (const char *)packed + i * pb, idx);
+        /* the one-hot row sets each x[j] once: sort, drop repeats */
+        for (int s = 1; s < k; ++s)
+            for (int t = s; t > 0 && idx[t - 1] > idx[t]; --t) {
+                const int tmp = idx[t];
+                idx[t] = idx[t - 1];
+                idx[t - 1] = tmp;
+            }
+        int u = 0;
+        for (int t = 0; t < k; ++t)
+            if (t == 0 || idx[t] != idx[t - 1]) idx[u++] = idx[t];
+        k = u;
+        for (int t = 0; t < k; ++t)
+            if (idx[t] < 0 || idx[t] >= m->F) rc = ORC_ERR_ARG; /* packed state encodes outside [0, F) */
+        if (rc != ORC_OK) break;
         int best = 0;
         for (int e = 0; e < m->E; ++e) {
-            for (int j = 0; j < m->F; ++j) a[j] = 0;
-            for (int t = 0; t < k; ++t) a[idx[t]] = 1;
             for (int l = 0; l <= m->L; ++l) {
                 const orc_mlp_layer *ly = &m->layers[e * (m->L + 1) + l];
+                if (l == 0) {
+                    /* x is one-hot: W x = the sum of the active columns (exact
+                     * integers, so identical to the dense product) */
+                    for (int o = 0; o < ly->out; ++o) nx[o] = ly->bias[o];
+                    for (int t = 0; t < k; ++t) {
+                        const int8_t *col = ly->WT + (size_t)idx[t] * ly->out;
+                        for (int o = 0; o < ly->out; ++o) nx[o] += col[o];
+                    }
+                }
                 for (int o = 0; o < ly->out; ++o) {
-                    int32_t acc = ly->bias[o];
-                    const int8_t *w = ly->W + (size_t)o * ly->in;
-                    for (int t = 0; t < ly->in; ++t) acc += (int32_t)w[t] * a[t];
+                    int32_t acc = nx[o];
+                    if (l > 0) {
+                        const int8_t *w = ly->W + (size_t)o * ly->in;
+                        int32_t dot = 0;
+                        for (int t = 0; t < ly->in; ++t) dot += (int32_t)w[t] * (int32_t)a[t];
+                        acc = ly->bias[o] + dot;
+                    }
                     if (l < m->L) {
                         int32_t v = acc >> ly->shift; /* arithmetic: floor division */
-                        nx[o] = v < 0 ? 0 : (v > 255 ? 255 : v);
+                        nx2[o] = v < 0 ? 0 : (v > 255 ? 255 : v);
                     } else {
                         lg[o] = (double)acc * (double)m->out_scale[e];
                     }
                 }
-                if (l < m->L) memcpy(a, nx, sizeof(int32_t) * ly->out);
+                if (l < m->L)
+                    for (int o = 0; o < ly->out; ++o) a[o] = (uint8_t)nx2[o];
             }
             if (logits_out) memcpy(logits_out + ((size_t)i * m->E + e) * m->C, lg, sizeof(double) * m->C);
             orc_softmax(lg, m->C, p);
@@ -331,6 +365,7 @@ static int mlp_eval_range(const orc_mlp *m, int domain, double q, const void *pa
     }
     free(a);
     free(nx);
+    free(nx2);
     free(lg);
     free(p);
     return rc;

@@ -24,6 +24,7 @@ typedef struct {
     int in, out, shift;
     int8_t *W;
     int32_t *bias;
+    int8_t *WT; /* layer 0 only: W transposed [in][out] (sparse one-hot input) */
 } orc_mlp_layer;
 
 typedef struct {

@@ -6,9 +6,8 @@ products plus the reference's own compiled readout
 batch_eval.hpp:98-168, heuristic.hpp:95-126) -- see make_golden_mlp.py.
 Here the oracle's C restatement (oracle/bida_oracle.c, the checker every GPU
 MLP test compares against) must reproduce them on the reference's own random
-walks: 100,000 states for H <= 512, a 10,000-state prefix for the H=1610
-models (the scalar oracle needs ~45 s per 100K states there; the GPU suite
-checks the CUDA path on all 100,000, tests/test_gpu_parity_scale.py)."""
+walks, 100,000 states per model (the GPU suite checks the CUDA path on the
+same 100,000, tests/test_gpu_parity_scale.py)."""
 from __future__ import annotations
 
 import glob
@@ -50,7 +49,7 @@ def test_cases_present():
 @pytest.mark.parametrize("name", CASES)
 def test_oracle_matches_pinned_golden(name, states):
     z, blob = load_case(name)
-    n = len(states) if "h1610" not in name else 10_000
+    n = len(states)
     E, C = int(z["ensemble"]), int(z["classes"])
     h, lg = Oracle().mlp_evaluate(blob, RC, float(z["q"]), states[:n], want_logits=True, E=E, Cc=C,
                                   threads=os.cpu_count() or 1)
