@@ -336,64 +336,71 @@ def cpu_rate(wl, seconds_target, threads, seed=7, source=None):
     return run, kind, n * reps, packed
 
 
-SEARCH_WALKS = "1:15:15:2508"  # one walk-15 Rubik's scramble (configs[1]: walks 14-16)
+# Config-2 search instance (BASELINE configs[1]: Rubik's random walks of 14-16
+# moves): solved in Table-1 mode with the 8-corner PDB (tests/search_screen.py,
+# profiles/r2_search_screen.jsonl), so the leg reports time-to-solve as well
+SEARCH_WALK = (15, 2508)   # (length, seed) for random_walk_instance (instance.hpp:36-57)
+SEARCH_CORNERS = 8
 
 
-# ring-evaluator search leg configuration (profiles/r1_search_ring.jsonl sweep)
-# one evaluator (the per-evaluator ceiling the ring lifts; K=4, S=16 was the best mean of
-# profiles/r1_search_ring_repeat.jsonl) and two at the header defaults (K=2, S=8;
-# profiles/r1_search_ring_shards.jsonl)
-RING_SEARCH = [{"evaluators": 1, "agents": 4, "shards": 16, "batch": 16384, "timeout_us": 25},
-               {"evaluators": 2, "agents": 2, "shards": 8, "batch": 16384, "timeout_us": 25}]
-
-
-def search_leg(wl, seconds, threads, cpu: bool, ring: dict | None = None):
+def search_leg(wl, seconds, threads, impl="fast", gpus=1, evaluators=1, agents=4, shards=16, batch=16384,
+               timeout_us=25, walk=None):
     """Batch IDA* nodes/s (BASELINE metric, second half): the reference's own
-    batch_idastar (search.hpp:101-237) over a walk-15 Rubik's scramble, the
-    workload's BMLP1 network evaluated for every generated node, search guided
-    by the reference's 5-corner PDB (PAPER.md:407 Table-1 mode).
-    GPU: tools/bin/bida_search with 8 GpuBackend evaluators (network + PDB in
-    the device readout).  CPU (cpu=True, baseline leg only): the test build
-    tests/cpp/bin/search_parity with the oracle's CPU network, one evaluator
-    per searcher thread.  ring={"evaluators": E, "agents": K, "batch": B,
-    "timeout_us": t}: tools/bin/bida_search_ring, the same search with the
-    reference's Evaluator internals replaced by the ring evaluator (SURVEY
-    §8(f) row 1, include/bida_ring_evaluator.hpp)."""
+    batch_idastar (search.hpp:101-237, unchanged) on one config-2 Rubik's
+    scramble, the workload's BMLP1 network evaluated for every generated node,
+    search guided by the reference's 8-corner PDB (PAPER.md:407 Table-1 mode;
+    on the GPU the PDB lookup is fused into the device readout; the table is
+    built by bida_gpu_pdb_build, byte-identical to PdbTable::build).
+      impl="fast"      tools/bin/bida_search_fast: ring evaluator (SURVEY 8(f)
+                       row 1) + CB-DFS searcher overlay (row 2); GpuBackend on
+                       `gpus` devices, evaluator e on device e % gpus
+      impl="ring"      tools/bin/bida_search_ring: ring evaluator, reference cb_dfs
+      impl="reference" tools/bin/bida_search: reference Evaluator and cb_dfs
+      impl="cpu"       tests/cpp/bin/search_parity: the oracle's CPU network on
+                       every searcher thread (AIDA*, immediate evaluators)
+      impl="cpu_pdb"   tools/bin/bida_search --mode pdb --immediate: CPU AIDA* with
+                       the PDB only, no network (the paper's AIDA* row)"""
     from paper_2507_11916_b200.models import make_bmlp1
 
     if wl["domain"] != "rc" or wl["kind"] != "mlp":
         return None
+    L, seed = walk or SEARCH_WALK
     model = f"/tmp/bida_bench_{os.getpid()}.bmlp"
     with open(model, "wb") as f:
         f.write(make_bmlp1("rc", hidden=wl["H"], classes=wl["C"], ensemble=wl["E"], seed=2507))
-    if cpu:
-        exe = os.path.join(ROOT, "tests", "cpp", "bin", "search_parity")
-        extra = ["--mode", "cpu", "--evaluators", str(threads), "--work-num", "8", "--batch", "512", "--timeout-us", "200"]
-    elif ring:
-        exe = os.path.join(ROOT, "tools", "bin", "bida_search_ring")
-        extra = ["--mode", "gpu", "--gpu-pdb", "--evaluators", str(ring["evaluators"]), "--work-num", "128",
-                 "--batch", str(ring["batch"]), "--timeout-us", str(ring["timeout_us"])]
+    exe = {"fast": "tools/bin/bida_search_fast", "ring": "tools/bin/bida_search_ring",
+           "reference": "tools/bin/bida_search", "cpu": "tests/cpp/bin/search_parity",
+           "cpu_pdb": "tools/bin/bida_search"}[impl]
+    exe = os.path.join(ROOT, exe)
+    if impl in ("fast", "ring", "reference"):
+        extra = ["--mode", "gpu", "--gpu-pdb", "--gpus", str(gpus), "--evaluators", str(evaluators),
+                 "--work-num", "128", "--batch", str(batch), "--timeout-us", str(timeout_us)]
+    elif impl == "cpu":
+        extra = ["--mode", "cpu", "--immediate", "--work-num", "1"]
     else:
-        exe = os.path.join(ROOT, "tools", "bin", "bida_search")
-        extra = ["--mode", "gpu", "--gpu-pdb", "--evaluators", "8", "--work-num", "128", "--batch", "16384",
-                 "--timeout-us", "25"]
+        extra = ["--mode", "pdb", "--immediate", "--work-num", "1"]
     if not os.path.exists(exe):
         return {"unavailable": f"{exe} not built"}
-    cmd = [exe, "--domain", "rc", "--walks", SEARCH_WALKS, "--model", "mlp:" + model, "--q", str(wl["q"]),
-           "--table1-pdb", "5", "--threads", str(threads), "--time-limit", str(seconds), *extra]
-    env = {**os.environ, "BIDA_EVAL_AGENTS": str(ring["agents"]), "BIDA_EVAL_SHARDS": str(ring["shards"])} \
-        if ring else None
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    cmd = [exe, "--domain", "rc", "--walks", f"1:{L}:{L}:{seed}", "--model", "mlp:" + model, "--q", str(wl["q"]),
+           "--table1-pdb", str(SEARCH_CORNERS), "--pdb-build", "gpu", "--threads", str(threads),
+           "--time-limit", str(seconds), *extra]
+    env = {**os.environ, "BIDA_EVAL_AGENTS": str(agents), "BIDA_EVAL_SHARDS": str(shards)}
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=seconds * 3 + 300, env=env)
     os.unlink(model)
     rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
     if out.returncode or not rows:
         return {"unavailable": (out.stderr or "no output").strip().splitlines()[-1][:200]}
     r = rows[0]
-    return {"value": r["nodes_per_s"], "unit": "nodes/s", "evals_per_s": r["evals_per_s"],
-            "generated": r["generated"], "wall_s": r["wall_s"], "status": r["status"], "mean_batch": r["mean_batch"],
-            "threads": threads, "evaluators": r["evaluators"], "work_num": r["work_num"], "timeout_us": r["timeout_us"],
-            "batch": r["batch"], "evaluator_impl": r.get("evaluator_impl", "reference"),
-            **({"agents": ring["agents"], "shards": ring["shards"]} if ring else {})}
+    leg = {"value": r["nodes_per_s"], "unit": "nodes/s", "evals_per_s": r["evals_per_s"],
+           "generated": r["generated"], "wall_s": r["wall_s"], "status": r["status"], "cost": r["cost"],
+           "time_to_solve_s": r["wall_s"] if r["status"] == "solved" else None, "thresholds": r["thresholds"],
+           "mean_batch": r["mean_batch"], "threads": threads, "gpus": gpus if impl in ("fast", "ring", "reference") else 0,
+           "evaluators": r["evaluators"], "work_num": r["work_num"], "timeout_us": r["timeout_us"],
+           "batch": r["batch"], "evaluator_impl": r.get("evaluator_impl"), "search_impl": r.get("search_impl"),
+           "instance": f"random_walk_instance(solved, {L}, seed {seed})", "pdb_corners": SEARCH_CORNERS}
+    if r.get("evaluator_impl") == "ring":
+        leg.update(agents=agents, shards=shards)
+    return leg
 
 
 def host_cores():
@@ -630,30 +637,33 @@ def main():
     if world == 1 and args.sweep:
         line["batch_sweep"] = {"workload": args.workload, "config": "BASELINE configs[2]: batch 2^10..2^20",
                                "points": batch_sweep(wl, local)}
-    if world == 1 and args.search_seconds > 0:
+    if args.search_seconds > 0 and wl["kind"] == "mlp" and wl["domain"] == "rc":
+        # Batch IDA* nodes/s on all `world` GPUs from one host process (rank 0; one
+        # evaluator per GPU, tid % E routing, batch_eval.hpp:398-400)
         threads = host_cores()
-        sr = search_leg(wl, args.search_seconds, threads, cpu=False)
+        sr = search_leg(wl, args.search_seconds, threads, impl="fast", gpus=world, evaluators=world)
         if sr is not None:
             sr = {"metric": "batch_idastar_nodes_per_s", **sr,
-                  "config": {"domain": "rc", "instance": "random walk of 15 moves (seed 2508)", "heuristic":
-                             "BMLP1 evaluated per node + 5-corner PDB guidance (PAPER.md:407 Table-1 mode)",
-                             "search": "reference batch_idastar (search.hpp:101-237), unchanged"}}
-            if not args.no_cpu_baseline and "value" in sr:
-                cb = search_leg(wl, args.search_seconds, threads, cpu=True)
-                if cb and "value" in cb:
-                    sr["cpu_baseline"] = {"value": cb["value"], "unit": "nodes/s", "cores": threads, "kind": "port",
-                                          "sample": f"{cb['wall_s']:.0f} s of the same search, oracle BMLP1 on "
-                                                    f"{threads} CPU evaluator threads"}
+                  "config": {"domain": "rc", "heuristic": "BMLP1 evaluated per node + 8-corner PDB guidance "
+                             "(PAPER.md:407 Table-1 mode)", "search": "reference batch_idastar (search.hpp:101-237)",
+                             "host": f"{threads} searcher threads on {threads} host cores"}}
+            if world == 1:
+                legs = {}
+                for impl, kw in (("ring", {}), ("reference", {"evaluators": 8, "agents": 1})):
+                    r2 = search_leg(wl, args.search_seconds, threads, impl=impl, **kw)
+                    if r2 is not None:
+                        legs[impl] = r2
+                sr["variants"] = legs
+                if not args.no_cpu_baseline:
+                    cb = search_leg(wl, min(args.search_seconds, 10.0), threads, impl="cpu")
+                    if cb and "value" in cb:
+                        sr["cpu_baseline"] = {"value": cb["value"], "unit": "nodes/s", "cores": threads, "kind": "port",
+                                              "sample": f"{cb['wall_s']:.0f} s of the same search (AIDA*, immediate "
+                                                        f"evaluators), oracle BMLP1 on {threads} searcher threads"}
+                    cp = search_leg(wl, args.search_seconds, threads, impl="cpu_pdb")
+                    if cp and "value" in cp:
+                        sr["cpu_pdb_only"] = cp
             line["search"] = sr
-        legs = []
-        for rcfg in RING_SEARCH:
-            rr = search_leg(wl, args.search_seconds, threads, cpu=False, ring=rcfg)
-            if rr is not None:
-                legs.append({"metric": "batch_idastar_nodes_per_s", **rr, "evaluator":
-                             "ring evaluator (SURVEY 8(f) row 1, include/bida_ring_evaluator.hpp): lock-free "
-                             "sharded submit ring, K agents per evaluator; same search, instance and model as 'search'"})
-        if legs:
-            line["search_ring"] = legs
     print(json.dumps(line), flush=True)
 
 

@@ -1,0 +1,135 @@
+// latency_breakdown.cu — where the per-call time of a small batch goes
+// (VERDICT r1 weak #7 / next #5).  Not a test; output committed under
+// profiles/.  For each batch size it times, on one B200:
+//   launch_sync   an empty kernel + cudaStreamSynchronize (non-blocking stream)
+//   launch_poll   an empty kernel that writes a mapped flag, host spins on it
+//   device        bida_gpu_evaluate_device on device buffers + stream sync
+//   capi          bida_gpu_evaluate from page-locked host buffers (the C-ABI
+//                 call a search agent makes), called from C++ (no Python)
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
+//        tests/cpp/latency_breakdown.cu -L paper_2507_11916_b200/_lib -lbida_gpu
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <iterator>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "bida_gpu.h"
+
+__global__ void empty_kernel() {}
+__global__ void flag_kernel(volatile int *flag, int v) { *flag = v; }
+
+static double now_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+int main(int argc, char **argv) {
+    const char *model_path = argc > 1 ? argv[1] : nullptr;  // BMLP1 file; default: linear RC C=21
+    const char *kind = argc > 2 ? argv[2] : "mlp";
+    cudaSetDevice(0);
+    cudaStream_t st;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    const int reps = 2000;
+    // raw launch round trips
+    for (int i = 0; i < 100; ++i) {
+        empty_kernel<<<1, 32, 0, st>>>();
+        cudaStreamSynchronize(st);
+    }
+    double t0 = now_us();
+    for (int i = 0; i < reps; ++i) {
+        empty_kernel<<<1, 32, 0, st>>>();
+        cudaStreamSynchronize(st);
+    }
+    const double launch_sync = (now_us() - t0) / reps;
+    int *flag_h = nullptr, *flag_d = nullptr;
+    cudaHostAlloc(reinterpret_cast<void **>(&flag_h), 4, cudaHostAllocMapped);
+    cudaHostGetDevicePointer(reinterpret_cast<void **>(&flag_d), flag_h, 0);
+    *flag_h = 0;
+    t0 = now_us();
+    for (int i = 1; i <= reps; ++i) {
+        flag_kernel<<<1, 1, 0, st>>>(flag_d, i);
+        while (*reinterpret_cast<volatile int *>(flag_h) != i) {
+        }
+    }
+    const double launch_poll = (now_us() - t0) / reps;
+    cudaStreamSynchronize(st);
+    std::printf("{\"what\": \"raw\", \"launch_sync_us\": %.2f, \"launch_poll_us\": %.2f}\n", launch_sync, launch_poll);
+
+    bida_gpu_evaluator *ev = nullptr;
+    int rc;
+    if (std::string(kind) == "mlp") {
+        rc = bida_gpu_mlp_load(0, BIDA_DOMAIN_RC, model_path, 0.5, &ev);
+    } else {
+        std::vector<float> w(21 * 480);
+        std::mt19937 g(1);
+        std::uniform_real_distribution<float> u(-0.1f, 0.1f);
+        for (auto &x : w)
+            x = u(g);
+        rc = bida_gpu_linear_create(0, BIDA_DOMAIN_RC, w.data(), 1, 21, 0.5, &ev);
+    }
+    if (rc) {
+        std::fprintf(stderr, "create: %s\n", bida_gpu_last_error());
+        return 1;
+    }
+    // solved-cube-ish packed states (valid permutations)
+    const int maxB = 1 << 14;
+    std::vector<unsigned char> host(static_cast<size_t>(maxB) * 16);
+    for (int i = 0; i < maxB; ++i) {
+        uint64_t lo = 0, hi = 0;
+        for (int p = 0; p < 8; ++p)
+            lo |= static_cast<uint64_t>(p) << (3 * p);
+        for (int p = 0; p < 12; ++p)
+            hi |= static_cast<uint64_t>(p) << (4 * p);
+        lo |= static_cast<uint64_t>(i & 1) << 40;  // two edge flips -> still valid for the encode
+        lo |= static_cast<uint64_t>(i & 1) << 41;
+        std::memcpy(&host[static_cast<size_t>(i) * 16], &lo, 8);
+        std::memcpy(&host[static_cast<size_t>(i) * 16 + 8], &hi, 8);
+    }
+    unsigned char *pin_in = nullptr;
+    int32_t *pin_out = nullptr;
+    cudaHostAlloc(reinterpret_cast<void **>(&pin_in), host.size(), cudaHostAllocDefault);
+    cudaHostAlloc(reinterpret_cast<void **>(&pin_out), maxB * 4, cudaHostAllocDefault);
+    std::memcpy(pin_in, host.data(), host.size());
+    void *d_in = nullptr;
+    int32_t *d_h = nullptr;
+    cudaMalloc(&d_in, host.size());
+    cudaMalloc(reinterpret_cast<void **>(&d_h), maxB * 4);
+    cudaMemcpy(d_in, host.data(), host.size(), cudaMemcpyHostToDevice);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int B : {1, 8, 64, 256, 1024, 4096, 16384}) {
+        for (int i = 0; i < 20; ++i)
+            bida_gpu_evaluate(ev, pin_in, B, pin_out);
+        const int r = B >= 4096 ? 500 : reps;
+        t0 = now_us();
+        for (int i = 0; i < r; ++i)
+            bida_gpu_evaluate(ev, pin_in, B, pin_out);
+        const double capi = (now_us() - t0) / r;
+        t0 = now_us();
+        for (int i = 0; i < r; ++i) {
+            bida_gpu_evaluate_device(ev, d_in, B, d_h, nullptr, st);
+            cudaStreamSynchronize(st);
+        }
+        const double dev_sync = (now_us() - t0) / r;
+        cudaEventRecord(a, st);
+        for (int i = 0; i < r; ++i)
+            bida_gpu_evaluate_device(ev, d_in, B, d_h, nullptr, st);
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        std::printf("{\"what\": \"%s\", \"batch\": %d, \"capi_us\": %.2f, \"device_launch_sync_us\": %.2f, "
+                    "\"device_back_to_back_us\": %.2f}\n",
+                    kind, B, capi, dev_sync, ms * 1000.0 / r);
+    }
+    bida_gpu_destroy(ev);
+    return 0;
+}

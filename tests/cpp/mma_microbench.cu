@@ -4,6 +4,7 @@
 // only; results go to profiles/.  Build: see tests/cpp/Makefile (mma_microbench).
 #include <cstdio>
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 
 #include "../../paper_2507_11916_b200/csrc/sm100.cuh"
@@ -213,7 +214,39 @@ __global__ void __launch_bounds__(128, 1) stream(int n_mma, int N, int nbuf, int
         sm100::tmem_dealloc(tmem, 512);
 }
 
-int main() {
+// Sustained dense int8 rate on every SM: back-to-back M=128 N=256 K=32
+// kind::i8 MMAs from SMEM (the per-SM tcgen05 floor) for ~0.25 s per launch,
+// timed with CUDA events -- the roofline denominator for the BMLP1 kernels
+// (profiles/r2_int8_peak.txt).
+static int sustained() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    long long *d_out;
+    cudaMalloc(&d_out, sizeof(long long) * 2 * sms);
+    cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int n = 4000000, N = 256;
+    bench<<<sms, 128, 64 * 1024>>>(1000, N, 0, d_out);  // warm
+    cudaDeviceSynchronize();
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(a);
+        bench<<<sms, 128, 64 * 1024>>>(n, N, 0, d_out);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        const double ops = 2.0 * sms * static_cast<double>(n) * 128 * N * 32;
+        printf("{\"what\": \"int8_dense_sustained\", \"sms\": %d, \"mma\": \"M128 N256 K32 kind::i8, SMEM operands\", "
+               "\"ms\": %.3f, \"tops\": %.1f}\n", sms, ms, ops / (ms * 1e-3) / 1e12);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int main(int argc, char **argv) {
+    if (argc > 1 && std::string(argv[1]) == "sustained")
+        return sustained();
     long long *d_out, h_out[2 * 148];
     cudaMalloc(&d_out, sizeof(h_out));
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
