@@ -339,7 +339,7 @@ def cpu_rate(wl, seconds_target, threads, seed=7, source=None):
 # Config-2 search instance (BASELINE configs[1]: Rubik's random walks of 14-16
 # moves): solved in Table-1 mode with the 8-corner PDB (tests/search_screen.py,
 # profiles/r2_search_screen.jsonl), so the leg reports time-to-solve as well
-SEARCH_WALK = (15, 2508)   # (length, seed) for random_walk_instance (instance.hpp:36-57)
+SEARCH_WALK = (14, 2508)   # (length, seed) for random_walk_instance (instance.hpp:36-57): cost 13, ~0.7 G nodes
 SEARCH_CORNERS = 8
 
 
@@ -559,8 +559,8 @@ def main():
                     help="skip the reference-model (rc-linear-e1-c21) leg of an N=1 run")
     ap.add_argument("--no-sweep", dest="sweep", action="store_false",
                     help="skip the batch-size sweep (BASELINE configs[2]) of an N=1 run")
-    ap.add_argument("--search-seconds", type=float, default=10.0,
-                    help="Batch IDA* nodes/s leg (RC MLP workloads, N=1); 0 disables")
+    ap.add_argument("--search-seconds", type=float, default=60.0,
+                    help="time limit of each Batch IDA* leg (RC MLP workloads); 0 disables")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = WORKLOADS[args.workload]

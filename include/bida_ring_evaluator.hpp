@@ -52,6 +52,15 @@
 #include <thread>
 #include <vector>
 
+#if __has_include(<nvtx3/nvToolsExt.h>)
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3 (SURVEY §5 tracing)
+#define BIDA_NVTX_PUSH(name) nvtxRangePushA(name)
+#define BIDA_NVTX_POP() nvtxRangePop()
+#else
+#define BIDA_NVTX_PUSH(name) ((void)0)
+#define BIDA_NVTX_POP() ((void)0)
+#endif
+
 namespace bida {
 
 // Opt-in marker for backends whose evaluate() may run on several agent threads
@@ -409,6 +418,7 @@ private:
 
     void process(const std::vector<Range> &ranges, std::size_t n, bool forced_partial,
                  std::vector<BatchItem<D>> &scratch, std::vector<std::int32_t> &vals) {
+        BIDA_NVTX_PUSH(forced_partial ? "ring flush (forced)" : "ring flush");
         vals.assign(n, 0);
         const Range &r0 = ranges.front();
         const bool in_place = ranges.size() == 1 && (r0.h & mask_) + r0.n <= ring_size_;
@@ -442,6 +452,7 @@ private:
         stats_.record_batch(n);
         if (forced_partial)
             ++stats_.forced_flushes;
+        BIDA_NVTX_POP();
     }
 
     std::unique_ptr<EvaluatorBackend<D>> backend_;

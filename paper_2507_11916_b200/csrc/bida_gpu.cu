@@ -3,6 +3,7 @@
 // pinned staging slots and streams so host<->device copies of chunk i+1
 // overlap the kernel of chunk i.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing without a tool attached
 
 #include <algorithm>
 #include <atomic>
@@ -645,8 +646,20 @@ int bida_gpu_mlp_load(int device, int domain, const char *path, double quantile,
     return bida_gpu_mlp_create_bmlp1(device, domain, buf.data(), buf.size(), quantile, out);
 }
 
+} // extern "C"
+
+namespace {
+struct NvtxRange {  // SURVEY §5 tracing: one range per C-ABI evaluate call
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+} // namespace
+
+extern "C" {
+
 int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t n, int32_t *h_out,
                              double *logits_out) {
+    NvtxRange nvtx(n <= kZeroCopyMax && !logits_out ? "bida_gpu_evaluate/zero_copy" : "bida_gpu_evaluate/staged");
     if (!ev)
         return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL evaluator");
     if (n < 0 || (n > 0 && (!packed || !h_out)))
@@ -787,6 +800,7 @@ int bida_gpu_evaluate(bida_gpu_evaluator *ev, const void *packed, int64_t n, int
 
 int bida_gpu_evaluate_device(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h,
                              double *d_logits, void *stream) {
+    NvtxRange nvtx("bida_gpu_evaluate_device");
     if (!ev)
         return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL evaluator");
     if (n < 0 || (n > 0 && (!d_packed || !d_h)))

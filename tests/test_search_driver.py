@@ -135,3 +135,58 @@ def test_evaluator_unit_semantics(impl):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
     assert "all checks passed" in out.stdout
+
+
+FAST = os.path.join(ROOT, "tools", "bin", "bida_search_fast")
+
+
+@pytest.mark.skipif(not os.path.exists(FAST), reason="tools/bin/bida_search_fast not built")
+@pytest.mark.parametrize("threads,work_num,timeout_us", [("4", "4", "200"), ("4", "8", "0"), ("3", "2", "-1"),
+                                                         ("1", "1", "0")])
+def test_fast_cbdfs_matches_reference_search(tmp_path, man3, threads, work_num, timeout_us):
+    """the CB-DFS searcher loop overlay (include/
+    bida_fast_cbdfs.hpp: no per-child path copy, pooled ticket slots, batched
+    shared counters) against the reference's cb_dfs (cbdfs.hpp:254-415), both
+    over the reference's CPU LinearModelBackend: identical costs, threshold
+    histories and non-final per-iteration counts; with one thread and one
+    subtree slot every iteration and the solution path itself are identical."""
+    g = np.load(os.path.join(ROOT, "tests", "golden", "instances.npz"))
+    inst = tmp_path / "stp8.txt"
+    inst.write_text("\n".join("stp 3 " + " ".join(str((int(v) >> (4 * c)) & 15) for c in range(9))
+                              for v in g["stp8_100"][:40]) + "\n")
+    args = ["--domain", "stp3", "--instances", str(inst), "--model", "linear:" + man3, "--mode", "cpu",
+            "--threads", threads, "--work-num", work_num, "--batch", "32", "--timeout-us", timeout_us]
+    rc, ref, err = run(args)
+    assert rc == 0, err
+    out = subprocess.run([FAST, *args], capture_output=True, text=True, timeout=300,
+                         env={**os.environ, "BIDA_EVAL_SHARDS": "4"})
+    assert out.returncode == 0, out.stderr
+    fast = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(ref) == len(fast) == 40
+    exact = threads == "1" and work_num == "1"
+    for a, b in zip(ref, fast):
+        assert a["search_impl"] == "reference" and b["search_impl"] == "fast"
+        assert a["status"] == b["status"] == "solved"
+        assert a["cost"] == b["cost"] and a["thresholds"] == b["thresholds"]
+        upto = len(a["iterations"]) if exact else len(a["iterations"]) - 1
+        assert [it[:3] for it in a["iterations"][:upto]] == [it[:3] for it in b["iterations"][:upto]]
+        assert len(b["solution"]) == b["cost"]
+        if exact:
+            assert a["solution"] == b["solution"]
+
+
+@pytest.mark.skipif(not os.path.exists(FAST), reason="tools/bin/bida_search_fast not built")
+def test_fast_cbdfs_rc_pdb_multi_evaluator():
+    """Rubik's walks, corner-PDB backend, 2 evaluators: same costs and
+    thresholds as the reference search."""
+    args = ["--domain", "rc", "--walks", "3:5:7:9", "--model", "mlp:/dev/null", "--mode", "pdb",
+            "--table1-pdb", "4", "--threads", "4", "--work-num", "8", "--batch", "64", "--timeout-us", "0",
+            "--evaluators", "2"]
+    rc, ref, err = run(args)
+    assert rc == 0, err
+    out = subprocess.run([FAST, *args], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    fast = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert [r["status"] for r in fast] == ["solved"] * 3
+    assert [r["cost"] for r in fast] == [r["cost"] for r in ref]
+    assert [r["thresholds"] for r in fast] == [r["thresholds"] for r in ref]
