@@ -89,6 +89,7 @@ struct MlpParams {
     long long sbytes;
     int stage_bytes;    // wide: bytes per weight/activation stage
     int bias_bytes;     // wide: whole bias vector staged in shared memory (0: read from global)
+    int l2hint;         // wide: evict_last L2 policy on scratch stores and stage copies
 };
 
 constexpr int kTraceSlots = 256;
@@ -158,7 +159,8 @@ struct Tracer {
 // memory at bias_s (the wide schedule: its L1 is too small to keep it).
 template <bool GLOBAL>
 __device__ __forceinline__ void requant_block(uint32_t t_row, int t0, const int32_t *bias, int o0, int n, int sh,
-                                              uint32_t sout, uint8_t *gout, int row, uint32_t bias_s = 0u) {
+                                              uint32_t sout, uint8_t *gout, int row, uint32_t bias_s = 0u,
+                                              uint64_t l2pol = 0) {
     for (int j = 0; j < n; j += 64) {
         const int m = min(64, n - j);
         int32_t r[4][16];
@@ -182,8 +184,13 @@ __device__ __forceinline__ void requant_block(uint32_t t_row, int t0, const int3
             for (int u = 0; u < 4; ++u)
                 w[u] = sm100::pack_sat_u8x4((r[q][u * 4 + 0] + b4[u].x) >> sh, (r[q][u * 4 + 1] + b4[u].y) >> sh,
                                             (r[q][u * 4 + 2] + b4[u].z) >> sh, (r[q][u * 4 + 3] + b4[u].w) >> sh);
-            if constexpr (GLOBAL)
-                sm100::st_global_v4(gout + (oc >> 5) * 4096 + ((oc >> 4) & 1) * 2048 + row * 16, w[0], w[1], w[2], w[3]);
+            if constexpr (GLOBAL) {
+                uint8_t *dst = gout + (oc >> 5) * 4096 + ((oc >> 4) & 1) * 2048 + row * 16;
+                if (l2pol)
+                    sm100::st_global_v4_hint(dst, w[0], w[1], w[2], w[3], l2pol);
+                else
+                    sm100::st_global_v4(dst, w[0], w[1], w[2], w[3]);
+            }
             else
                 sm100::st_shared_v4(sout + (oc >> 4) * 2048u + row * 16u, w[0], w[1], w[2], w[3]);
         }
@@ -768,6 +775,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
     if constexpr (PAIR)
         sm100::cluster_sync();  // peer barriers initialised before any remote arrive / multicast commit
     sm100::tc_fence_after();
+    const uint64_t l2pol = p.l2hint ? sm100::l2_policy_evict_last() : 0ull;
     const uint32_t tmem = *tmem_slot;
     Tracer tr;
     if (Tracer::kOn && p.trace && blockIdx.x == 0 && lane_id() == 0)
@@ -806,10 +814,17 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
                                 sm100::mbar_arrive_expect_tx(&full[s], abytes + kn * bb);
                                 if (PAIR && rank == 0)  // the peer relay's st.async signal for this stage
                                     sm100::mbar_arrive_expect_tx(&full2[s], 4u);
-                                if (l > 0)
-                                    sm100::bulk_g2s(st, a_src + kc * kWideStageA, abytes, &full[s]);
-                                sm100::bulk_g2s(st + (l > 0 ? ks * kWideStageA : 0), b_src + static_cast<long long>(kc) * bb,
-                                                kn * bb, &full[s]);
+                                if (p.l2hint) {  // scratch + weights: keep in L2 (evict_last)
+                                    if (l > 0)
+                                        sm100::bulk_g2s_hint(st, a_src + kc * kWideStageA, abytes, &full[s], l2pol);
+                                    sm100::bulk_g2s_hint(st + (l > 0 ? ks * kWideStageA : 0),
+                                                         b_src + static_cast<long long>(kc) * bb, kn * bb, &full[s], l2pol);
+                                } else {
+                                    if (l > 0)
+                                        sm100::bulk_g2s(st, a_src + kc * kWideStageA, abytes, &full[s]);
+                                    sm100::bulk_g2s(st + (l > 0 ? ks * kWideStageA : 0),
+                                                    b_src + static_cast<long long>(kc) * bb, kn * bb, &full[s]);
+                                }
                                 if (++s == p.stages) {
                                     s = 0;
                                     ph ^= 1u;
@@ -1019,7 +1034,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_wide_kernel(const __grid_c
                         if (hidden) {
                             const int half = cw >> 1;  // multiple of 16: widths are padded to 32
                             requant_block<true>(t_row, grp * half, bias, c0 + grp * half, half, ly.shift, 0u, out, row,
-                                                bias_s ? bias_s + ly.boff * 4u : 0u);
+                                                bias_s ? bias_s + ly.boff * 4u : 0u, l2pol);
                             sm100::tc_fence_before();
                             sm100::mbar_arrive(&tmem_free[b]);
                             tr(70 + l);
@@ -1362,6 +1377,10 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
         p.stage_bytes = wide_stage;
         p.bias_bytes = static_cast<int>(wide_bias_sm);
         p.cluster = wide_pair ? 2 : 1;
+        // evict_last L2 policy on the activation scratch and stage copies
+        // (BIDA_MLP_L2HINT=0 disables; profiles/r2_notes.md)
+        const char *hv = std::getenv("BIDA_MLP_L2HINT");
+        p.l2hint = !(hv && hv[0] == '0');
         m->smem = xwide + static_cast<size_t>(wide_stages) * wide_stage + wide_bias_sm + wide_bars;
     } else if (!want_split && fit_res && (fm.empty() || fm == "resident" || (fm == "pair" && !fit_pair))) {  // (TMEM double-buffered by job)
         p.mode = kResident;

@@ -88,7 +88,8 @@ def test_stp8_grid_matches_cpu(tmp_path, manhattan_blins):
 
 
 def test_korf_linear_manhattan_matches_cpu(tmp_path, manhattan_blins):
-    """Config 1: Korf #9 and #5 (costs 46, 56) with the linear-Manhattan model."""
+    """Config 1: Korf #9 (cost 46) with the linear-Manhattan model (the other
+    CPU-runnable Korf instances are in test_korf_config1_solved_parity)."""
     g = np.load(os.path.join(GOLDEN, "instances.npz"))
     inst = write_instances(tmp_path, "korf.txt", g["korf10"], "stp4")
     rows = run(["--domain", "stp4", "--instances", inst, "--model", "linear:" + manhattan_blins[1],
