@@ -343,6 +343,35 @@ SEARCH_WALK = (14, 2508)   # (length, seed) for random_walk_instance (instance.h
 SEARCH_CORNERS = 8
 
 
+def search_command(impl, model, q, seconds, threads, gpus, evaluators, batch, timeout_us, walk):
+    """argv of one Batch IDA* run (see search_leg).  GPU legs spread
+    `evaluators` GpuBackends over `gpus` devices (evaluator e on device
+    e % gpus, tools/bida_search.cpp) and route searcher thread tid to
+    evaluator tid % E (batch_eval.hpp:398-400)."""
+    L, seed = walk
+    exe = {"fast": "tools/bin/bida_search_fast", "ring": "tools/bin/bida_search_ring",
+           "reference": "tools/bin/bida_search", "cpu": "tests/cpp/bin/search_parity",
+           "cpu_pdb": "tools/bin/bida_search"}[impl]
+    if impl in ("fast", "ring", "reference"):
+        extra = ["--mode", "gpu", "--gpu-pdb", "--gpus", str(gpus), "--evaluators", str(evaluators),
+                 "--work-num", "128", "--batch", str(batch), "--timeout-us", str(timeout_us)]
+    elif impl == "cpu":
+        extra = ["--mode", "cpu", "--immediate", "--work-num", "1"]
+    else:
+        extra = ["--mode", "pdb", "--immediate", "--work-num", "1"]
+    return [os.path.join(ROOT, exe), "--domain", "rc", "--walks", f"1:{L}:{L}:{seed}", "--model", "mlp:" + model,
+            "--q", str(q), "--table1-pdb", str(SEARCH_CORNERS), "--pdb-build", "gpu", "--threads", str(threads),
+            "--time-limit", str(seconds), *extra]
+
+
+def search_plan(rank, world):
+    """The search legs of a bench run: rank 0 alone drives all `world` GPUs
+    from one host process (one evaluator per GPU); other ranks run none."""
+    if rank != 0:
+        return None
+    return {"impl": "fast", "gpus": world, "evaluators": world}
+
+
 def search_leg(wl, seconds, threads, impl="fast", gpus=1, evaluators=1, agents=4, shards=16, batch=16384,
                timeout_us=25, walk=None):
     """Batch IDA* nodes/s (BASELINE metric, second half): the reference's own
@@ -368,22 +397,9 @@ def search_leg(wl, seconds, threads, impl="fast", gpus=1, evaluators=1, agents=4
     model = f"/tmp/bida_bench_{os.getpid()}.bmlp"
     with open(model, "wb") as f:
         f.write(make_bmlp1("rc", hidden=wl["H"], classes=wl["C"], ensemble=wl["E"], seed=2507))
-    exe = {"fast": "tools/bin/bida_search_fast", "ring": "tools/bin/bida_search_ring",
-           "reference": "tools/bin/bida_search", "cpu": "tests/cpp/bin/search_parity",
-           "cpu_pdb": "tools/bin/bida_search"}[impl]
-    exe = os.path.join(ROOT, exe)
-    if impl in ("fast", "ring", "reference"):
-        extra = ["--mode", "gpu", "--gpu-pdb", "--gpus", str(gpus), "--evaluators", str(evaluators),
-                 "--work-num", "128", "--batch", str(batch), "--timeout-us", str(timeout_us)]
-    elif impl == "cpu":
-        extra = ["--mode", "cpu", "--immediate", "--work-num", "1"]
-    else:
-        extra = ["--mode", "pdb", "--immediate", "--work-num", "1"]
-    if not os.path.exists(exe):
-        return {"unavailable": f"{exe} not built"}
-    cmd = [exe, "--domain", "rc", "--walks", f"1:{L}:{L}:{seed}", "--model", "mlp:" + model, "--q", str(wl["q"]),
-           "--table1-pdb", str(SEARCH_CORNERS), "--pdb-build", "gpu", "--threads", str(threads),
-           "--time-limit", str(seconds), *extra]
+    cmd = search_command(impl, model, wl["q"], seconds, threads, gpus, evaluators, batch, timeout_us, (L, seed))
+    if not os.path.exists(cmd[0]):
+        return {"unavailable": f"{cmd[0]} not built"}
     env = {**os.environ, "BIDA_EVAL_AGENTS": str(agents), "BIDA_EVAL_SHARDS": str(shards)}
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=seconds * 3 + 300, env=env)
     os.unlink(model)
@@ -536,10 +552,22 @@ def roofline_for(name, wl, B, kern_avg_ms):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                 "algorithmic_bytes_per_state": by}
     achieved = fl * B / kern_s / 1e12
-    pk = peaks.get("bf16_tflops", 1590.0) * 2  # dense int8 = 2x dense bf16
+    # dense int8 peak MEASURED on this pool's B200s (profiles/r2_int8_peak.json,
+    # tests/int8_peak.py): back-to-back M128 N256 K32 tcgen05.mma kind::i8 on all
+    # 148 SMs for ~1 s (sustained clocks); cuBLAS int8 GEMM given beside it
+    pk, src, lib = None, None, None
+    ip = os.path.join(ROOT, "profiles", "r2_int8_peak.json")
+    if os.path.exists(ip):
+        j = json.load(open(ip))
+        pk, lib = j.get("int8_tcgen05_sustained_tops"), j.get("cublas_int8_tops")
+        src = "measured: tcgen05 kind::i8 sustained on 148 SMs (profiles/r2_int8_peak.json)"
+    if not pk:
+        pk = 4500.0
+        src = "fallback: B200_PROFILING.md dense 8-bit 4.5 POPS"
     return {"bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
             "frac": achieved / pk, "traffic": traffic, "traffic_source": traffic_src, "flops_per_state": fl,
-            "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x dense bf16 on B200)"}
+            "peak_source": src, "cublas_int8_tops": lib,
+            "frac_of_cublas_int8": achieved / lib if lib else None}
 
 
 def main():
@@ -641,7 +669,8 @@ def main():
         # Batch IDA* nodes/s on all `world` GPUs from one host process (rank 0; one
         # evaluator per GPU, tid % E routing, batch_eval.hpp:398-400)
         threads = host_cores()
-        sr = search_leg(wl, args.search_seconds, threads, impl="fast", gpus=world, evaluators=world)
+        plan = search_plan(rank, world)
+        sr = search_leg(wl, args.search_seconds, threads, **plan)
         if sr is not None:
             sr = {"metric": "batch_idastar_nodes_per_s", **sr,
                   "config": {"domain": "rc", "heuristic": "BMLP1 evaluated per node + 8-corner PDB guidance "

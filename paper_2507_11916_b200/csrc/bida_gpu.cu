@@ -136,6 +136,9 @@ constexpr int64_t kMaxSlot = int64_t(1) << 18;
 // states from mapped pinned memory and writes h straight back into it (one
 // launch + one stream sync per call; search batches are 1-8K states).
 constexpr int64_t kZeroCopyMax = int64_t(1) << 15;
+// linear thread kernel: at or below this many states the weights are not
+// staged in shared memory (profiles/r2_latency_breakdown_linear.jsonl)
+constexpr int64_t kLinSmallBatch = int64_t(1) << 12;
 
 template <int DOMAIN, int CS>
 int launch_linear_t(bida_gpu_evaluator *ev, const LinearArgs &a, cudaStream_t st) {
@@ -202,7 +205,10 @@ int launch_linear_thread(bida_gpu_evaluator *ev, const void *d_packed, int64_t n
     a.rk.thr = ev->thr;
     a.rk.uLo = ev->uLo;
     a.rk.uHi = ev->uHi;
-    a.w_in_smem = ev->w_in_smem;
+    // small batches (the search's zero-copy regime) read the weights through
+    // L1/L2 instead of staging the whole table into every CTA's shared memory
+    const bool small = n <= kLinSmallBatch;
+    a.w_in_smem = small ? 0 : ev->w_in_smem;
     a.err = err;
     a.replays = ev->d_replays;
     a.pdb = ev->pdb;
@@ -212,7 +218,7 @@ int launch_linear_thread(bida_gpu_evaluator *ev, const void *d_packed, int64_t n
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, ev->lin_grid_cap)));
     void *args[] = {&a};
     CUDA_TRY(cudaLaunchKernel(linear_thread_kernel_for(ev->domain, ev->lin_cm), dim3(grid), dim3(kLinThreads),
-                              args, ev->lin_smem, st));
+                              args, small ? 0 : ev->lin_smem, st));
     ev->launches.fetch_add(1, std::memory_order_relaxed);
     return BIDA_OK;
 }

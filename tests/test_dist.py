@@ -31,7 +31,13 @@ def _worker(rank, world, port, q):
     bench.barrier(w)
     # per-rank synthetic batches are independent shards (seeded by rank)
     packed = bida.random_walks("rc", 512, 0, 30, seed=1000 * rank)
-    q.put((rank, mx, bench.whole_job_rate(512, 3, w, mx), packed.tobytes()))
+    # the Batch IDA* leg: rank 0 alone drives every GPU (one evaluator each)
+    plan = bench.search_plan(r, w)
+    cmd = None
+    if plan:
+        cmd = bench.search_command(plan["impl"], "/tmp/m.bmlp", 0.5, 10, 16, plan["gpus"], plan["evaluators"],
+                                   16384, 25, bench.SEARCH_WALK)
+    q.put((rank, mx, bench.whole_job_rate(512, 3, w, mx), packed.tobytes(), plan, cmd))
     import torch.distributed as dist
 
     dist.destroy_process_group()
@@ -50,6 +56,11 @@ def test_two_rank_gloo_bench_plumbing():
     assert res[0][1] == res[1][1] == 20.0          # max over ranks
     assert res[0][2] == res[1][2] == 512 * 3 * 2 / 0.020
     assert res[0][3] != res[1][3]                    # disjoint shards
+    assert res[0][4] == {"impl": "fast", "gpus": 2, "evaluators": 2} and res[1][4] is None
+    cmd = res[0][5]
+    assert cmd[0].endswith("tools/bin/bida_search_fast")
+    assert cmd[cmd.index("--gpus") + 1] == "2" and cmd[cmd.index("--evaluators") + 1] == "2"
+    assert cmd[cmd.index("--table1-pdb") + 1] == "8" and "--gpu-pdb" in cmd
 
 
 def test_single_rank_rate():
