@@ -578,7 +578,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=0, help="states per GPU per step (default: workload's)")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample size (seconds of work)")
+    ap.add_argument("--cpu-seconds", type=float, default=6.0, help="CPU baseline sample size (seconds of work)")
     ap.add_argument("--ref-step-seconds", type=float, default=2.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-wide-leg", dest="wide_leg", action="store_false",
@@ -600,7 +600,15 @@ def main():
             print(json.dumps(line), flush=True)
         return
 
+    T0 = time.perf_counter()
+    timings = {}
+
+    def mark(name):
+        timings[name] = round(time.perf_counter() - T0, 1)
+        print(f"[bench] {name} done at {timings[name]} s", file=sys.stderr, flush=True)
+
     r = run_ours(args, wl, rank, world, local)
+    mark("headline")
     if rank != 0:
         return
     B = r["B"]
@@ -641,6 +649,7 @@ def main():
         # the north star's tensor-utilisation target refers to; device-resident only
         ww = WORKLOADS[WIDE_WORKLOAD]
         rw = run_ours(args, ww, rank, world, local, e2e=False)
+        mark("wide_model_run")
         line["wide_model"] = {
             "workload": WIDE_WORKLOAD, "model": {k: v for k, v in ww.items() if k in ("kind", "E", "C", "q", "H")},
             "value": whole_job_rate(rw["B"], args.steps, world, rw["total_ms"]), "unit": "evals/s",
@@ -648,6 +657,7 @@ def main():
             "roofline": roofline_for(WIDE_WORKLOAD, ww, rw["B"], rw["kern_avg_ms"]), "clocks": rw["clocks"]}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"], line["parity"] = cpu_baseline_and_parity(args, wl, r["host0"], local)
+        mark("cpu_baseline")
     if world == 1 and args.linear_leg and wl["kind"] != "linear":
         # the reference's own model (LinearModelBackend, BLIN1): device value, e2e,
         # roofline and its reference CPU baseline on the same timed batch
@@ -662,15 +672,18 @@ def main():
         if not args.no_cpu_baseline:
             leg["cpu_baseline"], leg["parity"] = cpu_baseline_and_parity(args, lw, rl["host0"], local)
         line["linear_model"] = leg
+        mark("linear_model")
     if world == 1 and args.sweep:
         line["batch_sweep"] = {"workload": args.workload, "config": "BASELINE configs[2]: batch 2^10..2^20",
                                "points": batch_sweep(wl, local)}
+        mark("batch_sweep")
     if args.search_seconds > 0 and wl["kind"] == "mlp" and wl["domain"] == "rc":
         # Batch IDA* nodes/s on all `world` GPUs from one host process (rank 0; one
         # evaluator per GPU, tid % E routing, batch_eval.hpp:398-400)
         threads = host_cores()
         plan = search_plan(rank, world)
         sr = search_leg(wl, args.search_seconds, threads, **plan)
+        mark("search_" + plan["impl"])
         if sr is not None:
             sr = {"metric": "batch_idastar_nodes_per_s", **sr,
                   "config": {"domain": "rc", "heuristic": "BMLP1 evaluated per node + 8-corner PDB guidance "
@@ -682,17 +695,21 @@ def main():
                     r2 = search_leg(wl, args.search_seconds, threads, impl=impl, **kw)
                     if r2 is not None:
                         legs[impl] = r2
+                    mark("search_" + impl)
                 sr["variants"] = legs
                 if not args.no_cpu_baseline:
                     cb = search_leg(wl, min(args.search_seconds, 10.0), threads, impl="cpu")
+                    mark("search_cpu")
                     if cb and "value" in cb:
                         sr["cpu_baseline"] = {"value": cb["value"], "unit": "nodes/s", "cores": threads, "kind": "port",
                                               "sample": f"{cb['wall_s']:.0f} s of the same search (AIDA*, immediate "
                                                         f"evaluators), oracle BMLP1 on {threads} searcher threads"}
-                    cp = search_leg(wl, args.search_seconds, threads, impl="cpu_pdb")
+                    cp = search_leg(wl, min(args.search_seconds, 30.0), threads, impl="cpu_pdb")
+                    mark("search_cpu_pdb")
                     if cp and "value" in cp:
                         sr["cpu_pdb_only"] = cp
             line["search"] = sr
+    line["bench_seconds"] = timings
     print(json.dumps(line), flush=True)
 
 

@@ -38,6 +38,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <memory>
 #include <thread>
 #include <vector>
@@ -45,6 +46,14 @@
 namespace bida {
 
 namespace fast_cbdfs {
+
+inline int idle_sleep_us() {
+    static const int us = [] {
+        const char *v = std::getenv("BIDA_SEARCH_IDLE_SLEEP_US");
+        return v ? std::atoi(v) : 0;
+    }();
+    return us;
+}
 
 // Per-thread pool of write-once ticket slots with stable addresses.
 class SlotPool {
@@ -277,8 +286,11 @@ void cb_dfs(int tid, int work_num, std::int64_t bound, WorkQueue<D> &queue, Eval
                 const int b = shared.blocked.fetch_add(1, std::memory_order_acq_rel) + 1;
                 if (b >= shared.running.load(std::memory_order_acquire))
                     group.kick_all();
-                if (++idle_cycles > 64)
-                    std::this_thread::sleep_for(std::chrono::microseconds(50));
+                // the reference sleeps 50 us after 64 idle cycles (cbdfs.hpp:392-395);
+                // on a device round trip of ~20 us that sleep is the latency, so
+                // the overlay only yields unless BIDA_SEARCH_IDLE_SLEEP_US says so
+                if (++idle_cycles > 64 && fast_cbdfs::idle_sleep_us() > 0)
+                    std::this_thread::sleep_for(std::chrono::microseconds(fast_cbdfs::idle_sleep_us()));
                 else
                     std::this_thread::yield();
                 shared.blocked.fetch_sub(1, std::memory_order_acq_rel);

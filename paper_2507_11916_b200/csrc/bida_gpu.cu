@@ -462,7 +462,12 @@ int linear_create_impl(int device, int domain, const float *weights, int E, int 
     if (C <= kLinMaxClasses && !ev->any_rowflag) {
         // thread-per-state kernel: [E][F+1][Cp], zero pad columns and a zero row F
         ev->lin_thread = true;
+        // row stride in 16-byte chunks made odd: the quarter-warp of a
+        // float4 load then spreads over all 8 bank groups (an even stride
+        // reaches only 4; profiles/r2_linear.txt: 72% LSU wavefront load)
         ev->Cp = (C + 3) & ~3;
+        if ((ev->Cp / 4) % 2 == 0)
+            ev->Cp += 4;
         ev->lin_cm = C <= 8 ? 8 : C <= 16 ? 16 : C <= 24 ? 24 : C <= 32 ? 32 : C <= 64 ? 64 : 96;
         const size_t per = static_cast<size_t>(F + 1) * ev->Cp;
         std::vector<float> w3(per * E, 0.0f);

@@ -60,7 +60,22 @@ int main(int argc, char **argv) {
     }
     const double launch_poll = (now_us() - t0) / reps;
     cudaStreamSynchronize(st);
-    std::printf("{\"what\": \"raw\", \"launch_sync_us\": %.2f, \"launch_poll_us\": %.2f}\n", launch_sync, launch_poll);
+    // back-to-back empty launches: host enqueue cost vs GPU-side time per launch
+    cudaEvent_t ea, eb;
+    cudaEventCreate(&ea);
+    cudaEventCreate(&eb);
+    cudaEventRecord(ea, st);
+    t0 = now_us();
+    for (int i = 0; i < reps; ++i)
+        empty_kernel<<<1, 32, 0, st>>>();
+    const double enqueue = (now_us() - t0) / reps;
+    cudaEventRecord(eb, st);
+    cudaEventSynchronize(eb);
+    float ems = 0;
+    cudaEventElapsedTime(&ems, ea, eb);
+    std::printf("{\"what\": \"raw\", \"launch_sync_us\": %.2f, \"launch_poll_us\": %.2f, "
+                "\"empty_enqueue_us\": %.2f, \"empty_back_to_back_gpu_us\": %.2f}\n",
+                launch_sync, launch_poll, enqueue, ems * 1000.0 / reps);
 
     bida_gpu_evaluator *ev = nullptr;
     int rc;
@@ -120,15 +135,17 @@ int main(int argc, char **argv) {
         }
         const double dev_sync = (now_us() - t0) / r;
         cudaEventRecord(a, st);
+        t0 = now_us();
         for (int i = 0; i < r; ++i)
             bida_gpu_evaluate_device(ev, d_in, B, d_h, nullptr, st);
+        const double enq = (now_us() - t0) / r;
         cudaEventRecord(b, st);
         cudaEventSynchronize(b);
         float ms = 0;
         cudaEventElapsedTime(&ms, a, b);
         std::printf("{\"what\": \"%s\", \"batch\": %d, \"capi_us\": %.2f, \"device_launch_sync_us\": %.2f, "
-                    "\"device_back_to_back_us\": %.2f}\n",
-                    kind, B, capi, dev_sync, ms * 1000.0 / r);
+                    "\"device_back_to_back_us\": %.2f, \"device_enqueue_us\": %.2f}\n",
+                    kind, B, capi, dev_sync, ms * 1000.0 / r, enq);
     }
     bida_gpu_destroy(ev);
     return 0;

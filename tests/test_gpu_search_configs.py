@@ -127,3 +127,20 @@ def test_config1_korf_linear_manhattan(korf, index, cost):
            cpu_nodes_per_s=c["nodes_per_s"])
     same_tree(g, c)
     assert g["cost"] == cost
+
+
+def test_two_evaluators_on_one_gpu_match(h128):
+    """The multi-GPU mapping on one device: two GpuBackend
+    evaluators (--evaluators 2 --gpus 1, evaluator e on device e % gpus, thread
+    tid routed to tid % 2, batch_eval.hpp:398-400) give the same tree as one."""
+    threads = str(len(os.sched_getaffinity(0)))
+    common = ["--domain", "rc", "--walks", "1:15:15:2522", "--model", "mlp:" + h128, "--q", "0.5",
+              "--table1-pdb", "8", "--pdb-build", "gpu", "--threads", threads, "--time-limit", "300",
+              "--mode", "gpu", "--gpu-pdb", "--work-num", "128", "--batch", "16384", "--timeout-us", "25"]
+    env = {"BIDA_EVAL_AGENTS": "2", "BIDA_EVAL_SHARDS": "8"}
+    one = run(FAST, [*common, "--evaluators", "1", "--gpus", "1"], env)
+    two = run(FAST, [*common, "--evaluators", "2", "--gpus", "1"], env)
+    assert two["evaluators"] == 2
+    record(config=2, length=15, seed=2522, evaluators=2, nodes_per_s_1=one["nodes_per_s"],
+           nodes_per_s_2=two["nodes_per_s"])
+    same_tree(two, one)
