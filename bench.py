@@ -199,7 +199,9 @@ def run_ours(args, wl, rank, world, local, e2e=True):
     pb = PACKED[wl["domain"]]
     # rotate input buffers whose total exceeds L2 so every step streams from HBM
     nbuf = max(2, int(np.ceil(2 * L2_BYTES / (B * pb))))
-    host = [bida.random_walks(wl["domain"], B, 0, 30, seed=1000 * rank + i) for i in range(min(nbuf, 2))]
+    # synthetic scrambles generated on the GPU (bida_gpu_random_walks), copied to the host
+    host = [bida.random_walks_fast(wl["domain"], B, 0, 30, seed=1000 * rank + i, device=local)
+            for i in range(min(nbuf, 2))]
     d_in = [torch.from_numpy(host[i % len(host)].view(np.uint8).copy()).to(dev) for i in range(nbuf)]
     d_h = [torch.empty(B, dtype=torch.int32, device=dev) for _ in range(nbuf)]
     be = make_backend(wl, local)
@@ -309,7 +311,7 @@ def cpu_rate(wl, seconds_target, threads, seed=7, source=None):
     import paper_2507_11916_b200 as bida
 
     # calibrate on a small sample, then size the sample to ~seconds_target
-    probe_n = 4096 if wl["kind"] == "linear" else 512
+    probe_n = 16384 if wl["kind"] == "linear" else 65536
     packed = bida.random_walks(wl["domain"], probe_n, 0, 30, seed=seed)
     run, kind = cpu_eval_fn(wl, packed, threads)
     t0 = time.perf_counter()
@@ -496,7 +498,7 @@ def batch_sweep(wl, local, sizes=None):
     stream = torch.cuda.current_stream()
     out = []
     for B in sizes:
-        host = bida.random_walks(wl["domain"], B, 0, 30, seed=B)
+        host = bida.random_walks_fast(wl["domain"], B, 0, 30, seed=B, device=local)
         d_in = torch.from_numpy(host.view(np.uint8).copy()).to(dev)
         d_h = torch.empty(B, dtype=torch.int32, device=dev)
         R = int(min(2000, max(20, (1 << 23) // B)))

@@ -146,6 +146,14 @@ int bida_gpu_pdb_build_save(int device, int domain, const uint8_t *pattern, int 
 /* Builds the table on the evaluator's device and attaches it (no host copy). */
 int bida_gpu_attach_pdb_built(bida_gpu_evaluator *ev, const uint8_t *pattern, int pattern_len, int mode);
 
+/* Synthetic benchmark input: n packed non-retracting random-walk
+ * scrambles from the solved state, state i of len_min + i % (len_max - len_min
+ * + 1) moves (the distribution of random_walk_instance, instance.hpp:36-57; a
+ * counter-based RNG, not mt19937_64), written to DEVICE memory d_out on
+ * `stream` (asynchronous). */
+int bida_gpu_random_walks(int device, int domain, int64_t n, int len_min, int len_max, uint64_t seed,
+                          void *d_out, void *stream);
+
 int bida_gpu_info(const bida_gpu_evaluator *ev, bida_gpu_model_info *out);
 /* Diagnostics (MLP handles): record a clock64 timeline of CTA 0's warps into
  * the DEVICE buffer `dev_buf` (int64 [32 warps][bida_gpu_trace_slots()]) on every

@@ -60,6 +60,7 @@ EXPORTS = [
     "bida_gpu_attach_pdb_built",
     "bida_gpu_pdb_build",
     "bida_gpu_pdb_build_save",
+    "bida_gpu_random_walks",
     "bida_gpu_info",
     "bida_gpu_debug_trace",
     "bida_gpu_trace_slots",
@@ -107,6 +108,7 @@ def lib() -> C.CDLL:
     L.bida_gpu_pdb_build.argtypes = [i32, i32, vp, i32, C.c_uint64, vp, C.c_uint64, C.POINTER(C.c_uint64),
                                      C.POINTER(i32)]
     L.bida_gpu_pdb_build_save.argtypes = [i32, i32, vp, i32, C.c_char_p]
+    L.bida_gpu_random_walks.argtypes = [i32, i32, i64, i32, i32, C.c_uint64, vp, vp]
     L.bida_gpu_info.argtypes = [H, C.POINTER(ModelInfo)]
     L.bida_gpu_debug_trace.argtypes = [H, vp]
     L.bida_gpu_exact_replays.argtypes = [H, C.POINTER(i64)]

@@ -256,3 +256,24 @@ def pdb_build_save(domain, pattern, path: str, device: int = 0) -> None:
     pat = np.ascontiguousarray(pattern, np.uint8)
     _native.check(_native.lib().bida_gpu_pdb_build_save(device, domain_id(domain), pat.ctypes.data_as(C.c_void_p),
                                                         len(pat), str(path).encode()))
+
+
+def random_walks_device(domain, n: int, len_min: int = 0, len_max: int = 30, seed: int = 0, device: int = 0):
+    """n packed random-walk scrambles generated on the GPU (bida_gpu_random_walks)
+    as a torch uint8 CUDA tensor of n * packed-bytes (synthetic benchmark input;
+    `random_walks` is the numpy equivalent with a different RNG)."""
+    import torch
+
+    d = domain_id(domain)
+    pb = 16 if d == 100 else 8
+    out = torch.empty(n * pb, dtype=torch.uint8, device=torch.device("cuda", device))
+    stream = torch.cuda.current_stream(device).cuda_stream
+    _native.check(_native.lib().bida_gpu_random_walks(device, d, n, len_min, len_max, seed,
+                                                      C.c_void_p(out.data_ptr()), C.c_void_p(stream)))
+    return out
+
+
+def random_walks_fast(domain, n: int, len_min: int = 0, len_max: int = 30, seed: int = 0, device: int = 0):
+    """Same, copied to a host numpy array of packed states."""
+    t = random_walks_device(domain, n, len_min, len_max, seed, device)
+    return t.cpu().numpy().view(packed_dtype(domain))

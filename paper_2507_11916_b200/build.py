@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libbida_gpu.so")
-SOURCES = ["bida_gpu.cu", "mlp.cu", "pdb_build.cu"]
+SOURCES = ["bida_gpu.cu", "mlp.cu", "pdb_build.cu", "walks.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
