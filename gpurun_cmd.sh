@@ -1,5 +1,5 @@
 cd "$(dirname "$0")"
-rm -f gpurun_out/korf_sweep.jsonl
-bash tests/korf_sweep.sh > gpurun_out/korf_sweep.log 2>&1
-timeout 900 python bench.py > gpurun_out/r2_bench2.json 2> gpurun_out/r2_bench2.err
-tests/cpp/bin/latency_breakdown none linear > gpurun_out/r2_latency_breakdown_linear2.jsonl 2>&1
+timeout 600 python -m pytest tests/test_gpu_walks.py tests/test_gpu_linear.py tests/test_gpu_search_configs.py -x -q > gpurun_out/r2_t3.log 2>&1
+timeout 900 python bench.py > gpurun_out/r2_bench3.json 2> gpurun_out/r2_bench3.err
+python tests/small_batch_launches.py > gpurun_out/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_small_launches.csv python tests/small_batch_launches.py > gpurun_out/ncu_small.log 2>&1

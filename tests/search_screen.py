@@ -105,7 +105,7 @@ def korf(args):
         with open(args.out, "a") as f:
             f.write(json.dumps({"korf": i, "side": "gpu", **gg}) + "\n")
         print("korf", i, "gpu", gg.get("status"), gg.get("cost"), gg.get("generated"), gg.get("wall_s"), flush=True)
-        c = run("bida_search", [*common, "--mode", "cpu", "--immediate", "--work-num", "1",
+        c = run("bida_search", [*common, "--mode", "cpu", "--immediate", "--work-num", "64",
                                 "--time-limit", str(args.cpu_limit)])
         same = (c.get("status") == "solved" and gg.get("status") == "solved" and c["cost"] == gg["cost"]
                 and c["thresholds"] == gg["thresholds"]

@@ -86,7 +86,9 @@ def test_config2_rubiks_walk_table1_8corner(h128, length, seed):
               "--table1-pdb", "8", "--pdb-build", "gpu", "--threads", threads, "--time-limit", "300"]
     g = run(FAST, [*common, "--mode", "gpu", "--gpu-pdb", "--work-num", "128", "--batch", "16384",
                    "--timeout-us", "25"], {"BIDA_EVAL_AGENTS": "4", "BIDA_EVAL_SHARDS": "16"})
-    c = run(REF, [*common, "--mode", "pdb", "--immediate", "--work-num", "1"])
+    # same threads and work_num: they fix d_init (search.hpp:61-79, >= 4 n k seeds), hence the
+    # split between work generation and the per-iteration counts
+    c = run(REF, [*common, "--mode", "pdb", "--immediate", "--work-num", "128"])
     record(config=2, length=length, seed=seed, cost=g["cost"], thresholds=g["thresholds"],
            gpu_generated=g["generated"], gpu_wall_s=g["wall_s"], gpu_nodes_per_s=g["nodes_per_s"],
            cpu_generated=c["generated"], cpu_wall_s=c["wall_s"], cpu_nodes_per_s=c["nodes_per_s"])
@@ -121,7 +123,7 @@ def test_config1_korf_linear_manhattan(korf, index, cost):
               "--first", str(index), "--count", "1", "--threads", threads, "--time-limit", "600"]
     g = run(FAST, [*common, "--mode", "gpu", "--work-num", "64", "--batch", "8192", "--timeout-us", "50"],
             {"BIDA_EVAL_AGENTS": "4", "BIDA_EVAL_SHARDS": "16"})
-    c = run(REF, [*common, "--mode", "cpu", "--immediate", "--work-num", "1"])
+    c = run(REF, [*common, "--mode", "cpu", "--immediate", "--work-num", "64"])
     record(config=1, korf=index, cost=g["cost"], gpu_generated=g["generated"], gpu_wall_s=g["wall_s"],
            gpu_nodes_per_s=g["nodes_per_s"], cpu_generated=c["generated"], cpu_wall_s=c["wall_s"],
            cpu_nodes_per_s=c["nodes_per_s"])
