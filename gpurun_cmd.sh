@@ -1,5 +1,5 @@
 cd "$(dirname "$0")"
-timeout 600 python -m pytest tests/test_gpu_walks.py tests/test_gpu_linear.py tests/test_gpu_search_configs.py -x -q > gpurun_out/r2_t3.log 2>&1
-timeout 900 python bench.py > gpurun_out/r2_bench3.json 2> gpurun_out/r2_bench3.err
-python tests/small_batch_launches.py > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_small_launches.csv python tests/small_batch_launches.py > gpurun_out/ncu_small.log 2>&1
+rm -f gpurun_out/search_configs.jsonl gpurun_out/parity_scale.jsonl gpurun_out/pdb_build.jsonl
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/r2_gputests_full.log 2>&1
+python tests/sanitizer_driver.py > gpurun_out/sanitizer_plain.log 2>&1 && \
+timeout 1200 compute-sanitizer --tool memcheck --target-processes all --print-limit 50 python tests/sanitizer_driver.py > gpurun_out/r2_sanitizer_memcheck.txt 2>&1
