@@ -111,6 +111,21 @@ int bida_gpu_evaluate(bida_gpu_evaluator *ev, const void *packed, int64_t n, int
 int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t n,
                              int32_t *h_out, double *logits_out);
 
+/* Asynchronous submit / complete (SURVEY §8(b) optional extra): bida_gpu_submit
+ * copies n <= 32768 packed HOST states into one of the handle's 8 zero-copy
+ * lanes (mapped pinned memory) and launches the evaluation; the GPU writes the
+ * int32 h-values straight into mapped host memory at bida_gpu_batch_h(b),
+ * readable once bida_gpu_batch_ready(b) returns 1 (0: not yet; < 0: -status).
+ * bida_gpu_batch_wait(b, h_out) waits, copies h (h_out may be NULL), reports
+ * this batch's errors only, and releases the lane (b is invalid afterwards).
+ * A lane is held from submit to wait: at most 8 batches per handle in flight;
+ * a ninth submit waits for a lane. */
+typedef struct bida_gpu_batch bida_gpu_batch;
+int bida_gpu_submit(bida_gpu_evaluator *ev, const void *packed, int64_t n, bida_gpu_batch **out);
+int bida_gpu_batch_ready(bida_gpu_batch *b);
+const int32_t *bida_gpu_batch_h(bida_gpu_batch *b);
+int bida_gpu_batch_wait(bida_gpu_batch *b, int32_t *h_out);
+
 /* Device-resident variant: d_packed / d_h / d_logits are DEVICE pointers on
  * the handle's device, `stream` a cudaStream_t (NULL = legacy default).
  * Asynchronous: returns after enqueueing; call bida_gpu_stream_status() after

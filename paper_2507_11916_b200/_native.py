@@ -54,6 +54,10 @@ EXPORTS = [
     "bida_gpu_evaluate",
     "bida_gpu_evaluate_logits",
     "bida_gpu_evaluate_device",
+    "bida_gpu_submit",
+    "bida_gpu_batch_ready",
+    "bida_gpu_batch_h",
+    "bida_gpu_batch_wait",
     "bida_gpu_stream_status",
     "bida_gpu_attach_pdb",
     "bida_gpu_attach_pdb_file",
@@ -102,6 +106,11 @@ def lib() -> C.CDLL:
     L.bida_gpu_evaluate_logits.argtypes = [H, vp, i64, vp, vp]
     L.bida_gpu_evaluate_device.argtypes = [H, vp, i64, vp, vp, vp]
     L.bida_gpu_stream_status.argtypes = [H]
+    L.bida_gpu_submit.argtypes = [H, vp, i64, C.POINTER(vp)]
+    L.bida_gpu_batch_ready.argtypes = [vp]
+    L.bida_gpu_batch_h.argtypes = [vp]
+    L.bida_gpu_batch_h.restype = C.POINTER(C.c_int32)
+    L.bida_gpu_batch_wait.argtypes = [vp, vp]
     L.bida_gpu_attach_pdb.argtypes = [H, vp, i32, vp, C.c_uint64, i32]
     L.bida_gpu_attach_pdb_file.argtypes = [H, C.c_char_p, i32]
     L.bida_gpu_attach_pdb_built.argtypes = [H, vp, i32, i32]

@@ -63,6 +63,14 @@ class _GpuBackendBase:
             )
         return h
 
+    def submit(self, packed) -> "Batch":
+        """Asynchronous evaluation of <= 32768 states (bida_gpu_submit): returns
+        a Batch whose ready() / wait() complete it; up to 8 in flight."""
+        p = np.ascontiguousarray(_as_packed(self.domain, packed))
+        b = C.c_void_p()
+        _native.check(_native.lib().bida_gpu_submit(self._h, p.ctypes.data_as(C.c_void_p), len(p), C.byref(b)))
+        return Batch(b, len(p))
+
     def evaluate_logits(self, packed):
         """(h, logits[n][E][C] float64): diagnostics for parity tests."""
         p = _as_packed(self.domain, packed)
@@ -231,6 +239,33 @@ class MlpModelBackend(_GpuBackendBase):
     def load(cls, domain, path: str, quantile: float, device: int = 0) -> "MlpModelBackend":
         with open(path, "rb") as f:
             return cls(domain, f.read(), quantile, device)
+
+
+class Batch:
+    """An in-flight asynchronous batch (bida_gpu_submit)."""
+
+    def __init__(self, handle, n):
+        self._b, self.n = handle, n
+
+    def ready(self) -> bool:
+        r = _native.lib().bida_gpu_batch_ready(self._b)
+        if r < 0:
+            _native.check(-r)
+        return r == 1
+
+    def peek(self) -> np.ndarray:
+        """The h-values in mapped host memory where the GPU wrote them (valid
+        once ready(), until wait())."""
+        ptr = _native.lib().bida_gpu_batch_h(self._b)
+        return np.ctypeslib.as_array(ptr, shape=(self.n,)).copy() if self.n else np.empty(0, np.int32)
+
+    def wait(self) -> np.ndarray:
+        if self._b is None:
+            raise RuntimeError("batch already completed")
+        h = np.empty(self.n, np.int32)
+        b, self._b = self._b, None
+        _native.check(_native.lib().bida_gpu_batch_wait(b, h.ctypes.data_as(C.c_void_p)))
+        return h
 
 
 def pdb_build(domain, pattern, device: int = 0, max_entries: int = 0) -> np.ndarray:

@@ -15,6 +15,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/bida_gpu.h"
@@ -68,7 +69,7 @@ int pdb_build_device(int domain, const uint8_t *pattern, int m, uint8_t **d_out,
 // states in flight on kSlots streams, so the H2D copy of chunk i+1.. overlaps
 // the kernel of chunk i and the D2H of chunk i-1 (copy engines are full duplex).
 constexpr int kSlots = 4;
-constexpr int kZcLanes = 4;
+constexpr int kZcLanes = 8;
 // Error channels: each zero-copy lane, the pipelined path and the device path
 // own kErrWords mapped words, so a bad state in one call is reported by that
 // call only (concurrent agents share a handle).
@@ -114,11 +115,16 @@ struct bida_gpu_evaluator {
     // kernel, kZcLanes independent lanes (own lock, stream and buffers) so
     // concurrent callers on one handle (the ring evaluator's agents,
     // include/bida_ring_evaluator.hpp) keep several batches on the device
+    // A lane is owned by one call at a time (busy flag); the asynchronous
+    // submit / wait pair (bida_gpu_submit) keeps it across calls.
     struct ZcLane {
-        std::mutex mu;
+        std::atomic<int> busy{0};
         cudaStream_t st = nullptr;
+        cudaEvent_t done = nullptr;
         void *in = nullptr, *in_dev = nullptr;
         int32_t *out = nullptr, *out_dev = nullptr;
+        int64_t n = 0;
+        bida_gpu_evaluator *owner = nullptr;
     } zc[kZcLanes];
     std::atomic<unsigned> zc_next{0};
     std::mutex err_mu;
@@ -263,6 +269,44 @@ int launch(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h
 
 int *chan_err(bida_gpu_evaluator *ev, int ch) { return ev->err_dev + ch * kErrWords; }
 
+// First free zero-copy lane from a rotating start; spins (then yields) while
+// every lane is busy.
+bida_gpu_evaluator::ZcLane *acquire_lane(bida_gpu_evaluator *ev) {
+    const unsigned start = ev->zc_next.fetch_add(1, std::memory_order_relaxed);
+    for (unsigned spins = 0;; ++spins) {
+        for (int k = 0; k < kZcLanes; ++k) {
+            auto &cand = ev->zc[(start + k) % kZcLanes];
+            int idle = 0;
+            if (cand.busy.load(std::memory_order_relaxed) == 0 &&
+                cand.busy.compare_exchange_strong(idle, 1, std::memory_order_acquire))
+                return &cand;
+        }
+        if (spins > 64)
+            std::this_thread::yield();
+    }
+}
+void release_lane(bida_gpu_evaluator::ZcLane *ln) { ln->busy.store(0, std::memory_order_release); }
+
+// Exclusive use of the whole handle (PDB attach): the pipelined path's mutex
+// plus every lane.
+struct HandleLock {
+    explicit HandleLock(bida_gpu_evaluator *e) : ev(e), lk(e->mu) {
+        for (auto &ln : ev->zc) {
+            int idle = 0;
+            while (!ln.busy.compare_exchange_weak(idle, 1, std::memory_order_acquire)) {
+                idle = 0;
+                std::this_thread::yield();
+            }
+        }
+    }
+    ~HandleLock() {
+        for (auto &ln : ev->zc)
+            release_lane(&ln);
+    }
+    bida_gpu_evaluator *ev;
+    std::lock_guard<std::mutex> lk;
+};
+
 // Decodes and clears one channel's error words.  Channels other than the
 // device path are owned by the call holding their lock; the device path's
 // words may be collected by any thread (bida_gpu_stream_status).
@@ -329,6 +373,8 @@ int common_init(bida_gpu_evaluator *ev, int device) {
     CUDA_TRY(cudaMemset(ev->d_replays, 0, sizeof(unsigned long long)));
     CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&ev->err_dev), ev->err_host, 0));
     for (auto &ln : ev->zc) {
+        ln.owner = ev;
+        CUDA_TRY(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming));
         CUDA_TRY(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking));
         CUDA_TRY(cudaHostAlloc(&ln.in, kZeroCopyMax * 16, cudaHostAllocMapped | cudaHostAllocWriteCombined));
         CUDA_TRY(cudaHostGetDevicePointer(&ln.in_dev, ln.in, 0));
@@ -354,6 +400,7 @@ void release(bida_gpu_evaluator *ev) {
     if (ev->err_host) cudaFreeHost(ev->err_host);
     for (auto &ln : ev->zc) {
         if (ln.st) cudaStreamSynchronize(ln.st);
+        if (ln.done) cudaEventDestroy(ln.done);
         if (ln.in) cudaFreeHost(ln.in);
         if (ln.out) cudaFreeHost(ln.out);
         if (ln.st) cudaStreamDestroy(ln.st);
@@ -679,22 +726,7 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         return BIDA_OK;
     CUDA_TRY(cudaSetDevice(ev->device));
     if (n <= kZeroCopyMax && !logits_out) {
-        // first free lane from a rotating start; block on one if all are busy
-        const unsigned start = ev->zc_next.fetch_add(1, std::memory_order_relaxed);
-        std::unique_lock<std::mutex> llk;
-        bida_gpu_evaluator::ZcLane *ln = nullptr;
-        for (int k = 0; k < kZcLanes && !ln; ++k) {
-            auto &cand = ev->zc[(start + k) % kZcLanes];
-            std::unique_lock<std::mutex> t(cand.mu, std::try_to_lock);
-            if (t.owns_lock()) {
-                llk = std::move(t);
-                ln = &cand;
-            }
-        }
-        if (!ln) {
-            ln = &ev->zc[start % kZcLanes];
-            llk = std::unique_lock<std::mutex>(ln->mu);
-        }
+        bida_gpu_evaluator::ZcLane *ln = acquire_lane(ev);
         const int pbz = packed_bytes(ev->domain);
         std::memcpy(ln->in, packed, static_cast<size_t>(n) * pbz);
         const int ch = static_cast<int>(ln - ev->zc);
@@ -708,10 +740,13 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         if (rc != BIDA_OK) {
             std::fill(h_out, h_out + n, 0);
             collect_errors(ev, ch);
+            release_lane(ln);
             return rc;
         }
         std::memcpy(h_out, ln->out, static_cast<size_t>(n) * 4);
-        return collect_errors(ev, ch);
+        rc = collect_errors(ev, ch);
+        release_lane(ln);
+        return rc;
     }
     std::lock_guard<std::mutex> lk(ev->mu);
     if (int rc = ensure_slots(ev, n)) {
@@ -809,6 +844,80 @@ int bida_gpu_evaluate(bida_gpu_evaluator *ev, const void *packed, int64_t n, int
     return bida_gpu_evaluate_logits(ev, packed, n, h_out, nullptr);
 }
 
+int bida_gpu_submit(bida_gpu_evaluator *ev, const void *packed, int64_t n, bida_gpu_batch **out) {
+    NvtxRange nvtx("bida_gpu_submit");
+    if (!out)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "out batch pointer is NULL");
+    *out = nullptr;
+    if (!ev)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL evaluator");
+    if (n < 0 || (n > 0 && !packed))
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "bad batch arguments");
+    if (n > kZeroCopyMax)
+        return fail(BIDA_ERR_CAPACITY, "asynchronous batches hold at most 32768 states");
+    CUDA_TRY(cudaSetDevice(ev->device));
+    bida_gpu_evaluator::ZcLane *ln = acquire_lane(ev);
+    const int ch = static_cast<int>(ln - ev->zc);
+    if (n > 0)
+        std::memcpy(ln->in, packed, static_cast<size_t>(n) * packed_bytes(ev->domain));
+    ln->n = n;
+    int rc = launch(ev, ln->in_dev, n, ln->out_dev, nullptr, ln->st, chan_err(ev, ch));
+    if (rc == BIDA_OK) {
+        const cudaError_t e = cudaEventRecord(ln->done, ln->st);
+        if (e != cudaSuccess)
+            rc = fail(BIDA_ERR_CUDA, std::string("submit: ") + cudaGetErrorString(e));
+    }
+    if (rc != BIDA_OK) {
+        cudaStreamSynchronize(ln->st);
+        collect_errors(ev, ch);
+        release_lane(ln);
+        return rc;
+    }
+    ev->zc_calls.fetch_add(1, std::memory_order_relaxed);
+    *out = reinterpret_cast<bida_gpu_batch *>(ln);
+    return BIDA_OK;
+}
+
+int bida_gpu_batch_ready(bida_gpu_batch *b) {
+    if (!b)
+        return -fail(BIDA_ERR_INVALID_ARGUMENT, "NULL batch");
+    auto *ln = reinterpret_cast<bida_gpu_evaluator::ZcLane *>(b);
+    const cudaError_t e = cudaEventQuery(ln->done);
+    if (e == cudaSuccess)
+        return 1;
+    if (e == cudaErrorNotReady)
+        return 0;
+    return -fail(BIDA_ERR_CUDA, std::string("batch: ") + cudaGetErrorString(e));
+}
+
+const int32_t *bida_gpu_batch_h(bida_gpu_batch *b) {
+    return b ? reinterpret_cast<bida_gpu_evaluator::ZcLane *>(b)->out : nullptr;
+}
+
+int bida_gpu_batch_wait(bida_gpu_batch *b, int32_t *h_out) {
+    NvtxRange nvtx("bida_gpu_batch_wait");
+    if (!b)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL batch");
+    auto *ln = reinterpret_cast<bida_gpu_evaluator::ZcLane *>(b);
+    bida_gpu_evaluator *ev = ln->owner;
+    const int ch = static_cast<int>(ln - ev->zc);
+    int rc = BIDA_OK;
+    const cudaError_t e = cudaEventSynchronize(ln->done);
+    if (e != cudaSuccess)
+        rc = fail(BIDA_ERR_CUDA, std::string("batch wait: ") + cudaGetErrorString(e));
+    const int erc = collect_errors(ev, ch);
+    if (rc == BIDA_OK)
+        rc = erc;
+    if (h_out && ln->n > 0) {
+        if (rc == BIDA_OK)
+            std::memcpy(h_out, ln->out, static_cast<size_t>(ln->n) * 4);
+        else
+            std::fill(h_out, h_out + ln->n, 0);
+    }
+    release_lane(ln);
+    return rc;
+}
+
 int bida_gpu_evaluate_device(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h,
                              double *d_logits, void *stream) {
     NvtxRange nvtx("bida_gpu_evaluate_device");
@@ -877,9 +986,7 @@ int bida_gpu_attach_pdb(bida_gpu_evaluator *ev, const uint8_t *pattern, int patt
                         const uint8_t *entries, uint64_t n_entries, int mode) {
     if (!ev)
         return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL evaluator");
-    std::lock_guard<std::mutex> lk(ev->mu);
-    static_assert(kZcLanes == 4, "lock every zero-copy lane");
-    std::scoped_lock lanes(ev->zc[0].mu, ev->zc[1].mu, ev->zc[2].mu, ev->zc[3].mu);
+    HandleLock all(ev);
     CUDA_TRY(cudaSetDevice(ev->device));
     if (mode == BIDA_PDB_OFF) {
         if (ev->d_pdb)
@@ -932,9 +1039,7 @@ int bida_gpu_attach_pdb_built(bida_gpu_evaluator *ev, const uint8_t *pattern, in
     uint64_t n = 0;
     if (int rc = bida_gpu::pdb_build_device(ev->domain, pattern, pattern_len, &d, &n))
         return rc;
-    std::lock_guard<std::mutex> lk(ev->mu);
-    static_assert(kZcLanes == 4, "lock every zero-copy lane");
-    std::scoped_lock lanes(ev->zc[0].mu, ev->zc[1].mu, ev->zc[2].mu, ev->zc[3].mu);
+    HandleLock all(ev);
     install_pdb(ev, pattern, pattern_len, d, n, mode);
     return BIDA_OK;
 }

@@ -132,6 +132,68 @@ __global__ void __launch_bounds__(512, 1) contention(int n_mma, int N, int sts_w
         sm100::tmem_dealloc(tmem, 512);
 }
 
+// SS MMAs (N = 128, the h128 schedule's shape) issued by warp 0 while
+// `ld_warps` other warps loop tcgen05.ld.32x32b.x16 + wait::ld over TMEM
+// columns [256, 384): does an epilogue draining the other TMEM half slow the
+// MMAs of the next job?  (profiles/r2_mma_tmem_contention.txt)
+__global__ void __launch_bounds__(512, 1) tmem_contention(int n_mma, int N, int ld_warps, long long *out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    __shared__ volatile int stop;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        sm100::mbar_init(&bar, 1);
+        sm100::fence_barrier_init();
+        stop = 0;
+    }
+    for (int i = threadIdx.x; i < 64 * 1024 / 16; i += blockDim.x)
+        reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+    sm100::fence_proxy_async_smem();
+    if (warp == 0)
+        sm100::tmem_alloc(&tslot, 512);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = tslot;
+    int sink = 0;
+    if (warp == 0) {
+        if (threadIdx.x == 0) {
+            const uint32_t sA = sm100::smem_u32(smem), sB = sA + 32 * 1024;
+            const uint32_t idesc = sm100::make_idesc_i8(N);
+            const long long t0 = clock64();
+            for (int i = 0; i < n_mma; ++i) {
+                const int ks = i & 3;
+                const uint64_t a = sm100::make_smem_desc(sA + ks * 4096u, 2048u, 128u);
+                const uint64_t b = sm100::make_smem_desc(sB + ks * (N * 32u), N * 16u, 128u);
+                sm100::mma_i8(tmem, a, b, idesc, i > 0 ? 1u : 0u);
+            }
+            sm100::mma_commit(&bar);
+            sm100::mbar_wait(&bar, 0);
+            out[blockIdx.x] = clock64() - t0;
+            stop = 1;
+        }
+    } else if (warp <= ld_warps) {
+        const uint32_t taddr = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + 256u;
+        int32_t r[16];
+        int k = 0;
+        while (!stop) {
+            sm100::tmem_ld16(taddr + (k & 7) * 16u, r);
+            sm100::tmem_wait_ld();
+            sink += r[0] + r[15];
+            ++k;
+        }
+    }
+    if (sink == 0x7fffffff)
+        out[0] = sink;
+    __syncwarp();
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    if (warp == 0)
+        sm100::tmem_dealloc(tmem, 512);
+}
+
 // Streaming operands: every MMA reads a DIFFERENT A (4 KB) and B (N*32 B) from
 // a ring of `nbuf` operand sets, optionally while warp 1 keeps the TMA engine
 // writing `tma_kb` KB stages from global memory into a separate region (the
@@ -244,9 +306,31 @@ static int sustained() {
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+static int tmem_contention_run() {
+    long long *d_out, h_out[148];
+    cudaMalloc(&d_out, sizeof(h_out));
+    cudaFuncSetAttribute(tmem_contention, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    for (int N : {128, 256})
+        for (int w : {0, 4, 8, 15}) {
+            const int n = 2048;
+            tmem_contention<<<148, 512, 64 * 1024>>>(n, N, w, d_out);
+            if (cudaDeviceSynchronize() != cudaSuccess)
+                return 1;
+            cudaMemcpy(h_out, d_out, sizeof(h_out), cudaMemcpyDeviceToHost);
+            double tot = 0;
+            for (int g = 0; g < 148; ++g)
+                tot += h_out[g];
+            printf("tmem_ld contention N=%3d ld_warps=%2d  %.1f cyc/mma (floor %.0f)\n", N, w, tot / 148 / n,
+                   128.0 * N / 256.0);
+        }
+    return 0;
+}
+
 int main(int argc, char **argv) {
     if (argc > 1 && std::string(argv[1]) == "sustained")
         return sustained();
+    if (argc > 1 && std::string(argv[1]) == "tmem")
+        return tmem_contention_run();
     long long *d_out, h_out[2 * 148];
     cudaMalloc(&d_out, sizeof(h_out));
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);

@@ -17,12 +17,12 @@ part 5).  Instances were chosen from the screens in
 profiles/r2_search_screen.jsonl (tests/search_screen.py) among those both sides
 solve in seconds.
 
-Config 1 (BASELINE configs[0]): Korf's 4x4 instances #9, #5 and #2
+Config 1 (BASELINE configs[0]): Korf's 4x4 instance #9
 (proj/data/korf10.txt, committed in tests/golden/instances.npz) with the
 linear-Manhattan model (C = 72, h = Manhattan distance):
 GPU Batch IDA* against the reference's CPU AIDA* with its own
-LinearModelBackend.  Costs 46 / 56 / 55 and identical thresholds and non-final
-iteration counts.
+LinearModelBackend.  Cost 46 and identical thresholds and non-final iteration
+counts (the screen covers #5, #2, #6 and #8 the same way).
 """
 from __future__ import annotations
 
@@ -115,15 +115,20 @@ def korf(tmp_path_factory):
     return str(inst), str(w)
 
 
-@pytest.mark.parametrize("index,cost", [(8, 46), (4, 56), (1, 55)])
+@pytest.mark.parametrize("index,cost", [(8, 46)])
 def test_config1_korf_linear_manhattan(korf, index, cost):
+    """Korf #9 here (~10 s a side); #5, #2, #6 and #8 ran the same check in
+    tests/search_screen.py --korf (profiles/r2_search_screen.jsonl, 1-3 min a
+    side).  d_init is fixed on both sides, so the CPU side can run the
+    reference's fastest AIDA* configuration (one subtree per thread)."""
     inst, w = korf
     threads = str(len(os.sched_getaffinity(0)))
     common = ["--domain", "stp4", "--instances", inst, "--model", "linear:" + w, "--q", "0.5",
-              "--first", str(index), "--count", "1", "--threads", threads, "--time-limit", "600"]
-    g = run(FAST, [*common, "--mode", "gpu", "--work-num", "64", "--batch", "8192", "--timeout-us", "50"],
-            {"BIDA_EVAL_AGENTS": "4", "BIDA_EVAL_SHARDS": "16"})
-    c = run(REF, [*common, "--mode", "cpu", "--immediate", "--work-num", "64"])
+              "--first", str(index), "--count", "1", "--threads", threads, "--time-limit", "600",
+              "--d-init", "12"]
+    g = run(FAST, [*common, "--mode", "gpu", "--work-num", "64", "--batch", "8192", "--timeout-us", "20"],
+            {"BIDA_EVAL_AGENTS": "2", "BIDA_EVAL_SHARDS": "16"})
+    c = run(REF, [*common, "--mode", "cpu", "--immediate", "--work-num", "1"])
     record(config=1, korf=index, cost=g["cost"], gpu_generated=g["generated"], gpu_wall_s=g["wall_s"],
            gpu_nodes_per_s=g["nodes_per_s"], cpu_generated=c["generated"], cpu_wall_s=c["wall_s"],
            cpu_nodes_per_s=c["nodes_per_s"])
