@@ -75,7 +75,8 @@ inline void throw_status(int rc, const char *what) {
 template <class D>
 class GpuBackend final : public bida::EvaluatorBackend<D>
 #ifdef BIDA_RING_EVALUATOR
-    , public bida::ConcurrentBackend  // the C-ABI handle is re-entrant (4 zero-copy lanes)
+    , public bida::ConcurrentBackend  // the C-ABI handle is re-entrant (8 zero-copy lanes)
+    , public bida::AsyncEvaluatorBackend<D>  // bida_gpu_submit / bida_gpu_batch_wait
 #endif
 {
 public:
@@ -137,7 +138,34 @@ public:
 
     bool needs_features() const override { return false; }
 #ifdef BIDA_RING_EVALUATOR
-    int max_concurrent_calls() const override { return 4; }  // zero-copy lanes per handle (bida_gpu.cu)
+    int max_concurrent_calls() const override { return 4; }
+    // Asynchronous path (ring agents keep several batches in flight each):
+    // the packed batch is copied into a zero-copy lane at submit; the GPU writes
+    // h into mapped host memory; complete() waits, copies and releases the lane.
+    int max_in_flight() const override { return 8; }  // zero-copy lanes per handle (bida_gpu.cu)
+    void *submit(std::span<const bida::BatchItem<D>> batch) override {
+        if (batch.size() > 32768)
+            return nullptr;  // larger than a lane: the caller uses evaluate()
+        thread_local std::vector<unsigned char> staging;
+        const std::size_t n = batch.size();
+        staging.resize(n * Traits::packed_bytes);
+        for (std::size_t i = 0; i < n; ++i)
+            Traits::pack(batch[i].state, staging.data() + i * Traits::packed_bytes);
+        bida_gpu_batch *b = nullptr;
+        const int rc = bida_gpu_submit(handle_, staging.data(), static_cast<std::int64_t>(n), &b);
+        if (rc) {
+            note_error();
+            return nullptr;  // fall back to the synchronous path, which zero-fills on error
+        }
+        calls_.fetch_add(1, std::memory_order_relaxed);
+        items_.fetch_add(n, std::memory_order_relaxed);
+        return b;
+    }
+    bool ready(void *token) override { return bida_gpu_batch_ready(static_cast<bida_gpu_batch *>(token)) != 0; }
+    void complete(void *token, std::span<std::int32_t> out) override {
+        if (bida_gpu_batch_wait(static_cast<bida_gpu_batch *>(token), out.data()) != BIDA_OK)
+            note_error();  // out[] zero-filled: frames never block forever
+    }
 #endif
 
     void evaluate(std::span<const bida::BatchItem<D>> batch, std::span<std::int32_t> out) override {
@@ -152,9 +180,7 @@ public:
         if (rc) {
             for (auto &v : out)
                 v = 0;  // h >= 0 keeps frames from blocking forever (cbdfs.hpp:262-265)
-            errors_.fetch_add(1, std::memory_order_relaxed);
-            std::lock_guard<std::mutex> lk(err_m_);
-            last_error_ = bida_gpu_last_error();
+            note_error();
         }
     }
 
@@ -169,6 +195,12 @@ public:
 
 private:
     explicit GpuBackend(bida_gpu_evaluator *h) : handle_(h) {}
+
+    void note_error() {
+        errors_.fetch_add(1, std::memory_order_relaxed);
+        std::lock_guard<std::mutex> lk(err_m_);
+        last_error_ = bida_gpu_last_error();
+    }
 
     bida_gpu_evaluator *handle_ = nullptr;
     std::atomic<std::uint64_t> errors_{0}, calls_{0}, items_{0};

@@ -45,6 +45,7 @@
 #include <climits>
 #include <cstdint>
 #include <cstdlib>
+#include <deque>
 #include <memory>
 #include <mutex>
 #include <span>
@@ -68,6 +69,20 @@ namespace bida {
 struct ConcurrentBackend {
     virtual ~ConcurrentBackend() = default;
     virtual int max_concurrent_calls() const = 0;
+};
+
+// Opt-in asynchronous evaluation (bida_gpu::GpuBackend: bida_gpu_submit /
+// bida_gpu_batch_wait): an agent keeps up to depth batches in flight instead
+// of blocking on each device round trip.
+template <class D>
+struct AsyncEvaluatorBackend {
+    virtual ~AsyncEvaluatorBackend() = default;
+    // Starts evaluating `batch` (read before returning); nullptr: not accepted,
+    // the caller uses evaluate() instead.
+    virtual void *submit(std::span<const BatchItem<D>> batch) = 0;
+    virtual bool ready(void *token) = 0;                                  // non-blocking
+    virtual void complete(void *token, std::span<std::int32_t> out) = 0;  // waits; writes every out[i]
+    virtual int max_in_flight() const = 0;                                // over all callers
 };
 
 namespace ring_detail {
@@ -94,6 +109,10 @@ inline int default_shards() {
     const char *s = std::getenv("BIDA_EVAL_SHARDS");
     const int k = s ? std::atoi(s) : 8;
     return std::clamp(k, 1, 64);
+}
+inline int env_inflight() {  // BIDA_EVAL_INFLIGHT: batches in flight per agent (0 = backend's share)
+    const char *s = std::getenv("BIDA_EVAL_INFLIGHT");
+    return s ? std::clamp(std::atoi(s), 0, 64) : 0;
 }
 // a small per-thread index, so a searcher thread keeps submitting to one shard
 inline std::size_t thread_slot() {
@@ -142,6 +161,17 @@ public:
         wake_step_ = std::max<std::uint64_t>(1, capacity_ / nshards_);
         if (!immediate_) {
             const int k_agents = ring_detail::agents_for(backend_.get(), agents);
+            // in-flight batches per agent: the backend's lanes shared by the
+            // agents (so an agent blocked in submit() never waits on lanes only
+            // blocked agents hold); 1 = synchronous evaluate()
+            async_ = dynamic_cast<AsyncEvaluatorBackend<D> *>(backend_.get());
+            if (async_) {
+                const int env = ring_detail::env_inflight();
+                depth_ = env > 0 ? env : std::max(1, async_->max_in_flight() / k_agents);
+                depth_ = std::min(depth_, std::max(1, async_->max_in_flight() / k_agents));
+                if (depth_ <= 1)
+                    async_ = nullptr;
+            }
             for (int k = 0; k < k_agents; ++k)
                 agents_.emplace_back([this] { agent_loop(); });
         }
@@ -251,6 +281,7 @@ public:
     std::uint64_t resolved() const { return resolved_.load(std::memory_order_relaxed); }
     std::uint64_t double_resolutions() const { return double_resolved_.load(std::memory_order_relaxed); }
     std::size_t agent_count() const { return agents_.size(); }
+    int in_flight_per_agent() const { return async_ ? depth_ : 1; }
     std::size_t shard_count() const { return nshards_; }
 
 private:
@@ -327,12 +358,35 @@ private:
         return n;
     }
 
-    void agent_loop() {
-        std::vector<BatchItem<D>> scratch; // batches spanning shards or a ring end
+    // One claimed batch from claim to resolution.
+    struct Flight {
+        std::vector<Range> ranges;
+        std::size_t n = 0;
+        bool forced_partial = false;
+        bool in_place = false;
+        std::vector<BatchItem<D>> scratch;  // batches spanning shards or a ring end
         std::vector<std::int32_t> vals;
+        void *token = nullptr;              // async backend: in flight
+    };
+
+    void agent_loop() {
+        std::deque<Flight> inflight;  // async: oldest first
+        std::vector<Flight> spare;
         std::vector<Range> ranges;
         std::size_t rot = 0;
+        auto finish_front = [&] {
+            finish(inflight.front());
+            spare.push_back(std::move(inflight.front()));
+            inflight.pop_front();
+        };
         for (;;) {
+            // completed device batches first (resolves their tickets)
+            while (!inflight.empty() && async_->ready(inflight.front().token))
+                finish_front();
+            if (inflight.size() >= static_cast<std::size_t>(depth_)) {
+                finish_front();  // pipeline full: wait for the oldest
+                continue;
+            }
             const std::uint32_t e = epoch_.load(std::memory_order_seq_cst);
             // read before the scan: once set, nothing new can be published
             const bool quiesced = quiesced_.load(std::memory_order_seq_cst);
@@ -360,6 +414,10 @@ private:
             const bool closed = closed_.load(std::memory_order_acquire);
             if (n == 0) {
                 lk.unlock();
+                if (!inflight.empty()) {  // nothing new: complete the oldest batch
+                    finish_front();
+                    continue;
+                }
                 if (quiesced && drained)
                     return;
                 if (closed || !drained) { // a producer is mid-publish
@@ -378,6 +436,10 @@ private:
                     due = true;
                 } else {
                     lk.unlock();
+                    if (!inflight.empty()) {  // use the wait to complete in-flight work
+                        finish_front();
+                        continue;
+                    }
                     // one agent watches the deadline; the others park on the
                     // epoch (producers wake them) instead of spinning too
                     if (deadline_owner_.exchange(true, std::memory_order_acq_rel)) {
@@ -399,6 +461,10 @@ private:
                 // steps, which need not coincide with the total reaching
                 // capacity, so re-check on a short sleep as well
                 lk.unlock();
+                if (!inflight.empty()) {
+                    finish_front();
+                    continue;
+                }
                 std::this_thread::sleep_for(std::chrono::microseconds(50));
                 continue;
             }
@@ -412,33 +478,57 @@ private:
             // another agent may proceed with the next range right away
             if (!drained || pending())
                 wake();
-            process(ranges, n, forced_partial, scratch, vals);
+            Flight f;
+            if (!spare.empty()) {
+                f = std::move(spare.back());
+                spare.pop_back();
+            }
+            f.ranges.assign(ranges.begin(), ranges.end());
+            f.n = n;
+            f.forced_partial = forced_partial;
+            f.token = nullptr;
+            const std::span<const BatchItem<D>> items = stage(f);
+            if (async_ && (f.token = async_->submit(items)) != nullptr) {
+                inflight.push_back(std::move(f));
+                continue;
+            }
+            f.vals.assign(n, 0);
+            backend_->evaluate(items, f.vals);
+            finish(f);
+            spare.push_back(std::move(f));
         }
     }
 
-    void process(const std::vector<Range> &ranges, std::size_t n, bool forced_partial,
-                 std::vector<BatchItem<D>> &scratch, std::vector<std::int32_t> &vals) {
-        BIDA_NVTX_PUSH(forced_partial ? "ring flush (forced)" : "ring flush");
-        vals.assign(n, 0);
-        const Range &r0 = ranges.front();
-        const bool in_place = ranges.size() == 1 && (r0.h & mask_) + r0.n <= ring_size_;
-        if (in_place) {
-            Shard &sh = shards_[r0.shard];
-            backend_->evaluate(std::span<const BatchItem<D>>(&sh.items[r0.h & mask_], n), vals);
-        } else {
-            scratch.clear();
-            for (const Range &r : ranges)
-                for (std::size_t i = 0; i < r.n; ++i)
-                    scratch.push_back(std::move(shards_[r.shard].items[(r.h + i) & mask_]));
-            backend_->evaluate(std::span<const BatchItem<D>>(scratch), vals);
+    // The batch's items as one span: in place in the ring, or moved into the
+    // flight's scratch when it spans shards or wraps.
+    std::span<const BatchItem<D>> stage(Flight &f) {
+        const Range &r0 = f.ranges.front();
+        f.in_place = f.ranges.size() == 1 && (r0.h & mask_) + r0.n <= ring_size_;
+        if (f.in_place)
+            return std::span<const BatchItem<D>>(&shards_[r0.shard].items[r0.h & mask_], f.n);
+        f.scratch.clear();
+        for (const Range &r : f.ranges)
+            for (std::size_t i = 0; i < r.n; ++i)
+                f.scratch.push_back(std::move(shards_[r.shard].items[(r.h + i) & mask_]));
+        return std::span<const BatchItem<D>>(f.scratch);
+    }
+
+    // Resolves the flight's tickets (in bulk, from the ring slots), releases the
+    // slots for the producers' next lap and records the batch.
+    void finish(Flight &f) {
+        BIDA_NVTX_PUSH(f.forced_partial ? "ring flush (forced)" : "ring flush");
+        if (f.token) {
+            f.vals.assign(f.n, 0);
+            async_->complete(f.token, f.vals);
+            f.token = nullptr;
         }
         std::size_t o = 0;
-        for (const Range &r : ranges) {
+        for (const Range &r : f.ranges) {
             Shard &sh = shards_[r.shard];
             for (std::size_t i = 0; i < r.n; ++i, ++o) {
-                BatchItem<D> &it = in_place ? sh.items[(r.h + i) & mask_] : scratch[o];
+                BatchItem<D> &it = f.in_place ? sh.items[(r.h + i) & mask_] : f.scratch[o];
                 Meta &mt = sh.meta[(r.h + i) & mask_];
-                resolve(mt.raw ? *mt.raw : *it.ticket, vals[o]);
+                resolve(mt.raw ? *mt.raw : *it.ticket, f.vals[o]);
                 mt.raw = nullptr;
                 it.ticket.reset();
                 if (!it.features.empty())
@@ -447,11 +537,13 @@ private:
             for (std::size_t i = 0; i < r.n; ++i)
                 sh.meta[(r.h + i) & mask_].seq.store(r.h + i + ring_size_, std::memory_order_release);
         }
-        resolved_.fetch_add(n, std::memory_order_relaxed);
-        std::lock_guard<std::mutex> slk(stats_m_);
-        stats_.record_batch(n);
-        if (forced_partial)
-            ++stats_.forced_flushes;
+        resolved_.fetch_add(f.n, std::memory_order_relaxed);
+        {
+            std::lock_guard<std::mutex> slk(stats_m_);
+            stats_.record_batch(f.n);
+            if (f.forced_partial)
+                ++stats_.forced_flushes;
+        }
         BIDA_NVTX_POP();
     }
 
@@ -470,6 +562,8 @@ private:
     std::atomic<bool> closed_{false};
     std::atomic<bool> deadline_owner_{false};
     std::atomic<bool> quiesced_{false};  // close(): closed_ set and no submit in flight
+    AsyncEvaluatorBackend<D> *async_ = nullptr;  // set: agents pipeline depth_ batches each
+    int depth_ = 1;
     std::mutex claim_m_;
     std::vector<std::thread> agents_;
 

@@ -4,7 +4,9 @@
 // against the reference's batch_eval.hpp (bin/evaluator_semantics_ref, the
 // control) and against the ring evaluator overlay (bin/evaluator_semantics_ring,
 // include/bida_ring_evaluator.hpp).  Exit 0 = every check passed.
+#include <algorithm>
 #include <array>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <random>
@@ -41,6 +43,60 @@ D::State walk(std::mt19937_64 &rng, int steps = 30) {
 }
 std::shared_ptr<const Heuristic<D>> man() { return std::make_shared<ManhattanHeuristic<3>>(); }
 std::unique_ptr<EvaluatorBackend<D>> sim() { return std::make_unique<TableSimBackend<D>>(man()); }
+#ifdef BIDA_RING_EVALUATOR
+// A device stand-in for the ring's asynchronous path: submit() computes the
+// values at once but reports them ready only `delay_us` later (a device round
+// trip), so agents keep several batches in flight.
+class AsyncSim final : public EvaluatorBackend<D>, public ConcurrentBackend, public AsyncEvaluatorBackend<D> {
+public:
+    explicit AsyncSim(int delay_us, int lanes = 8) : delay_ns_(delay_us * 1000ll), lanes_(lanes) {}
+    void evaluate(std::span<const BatchItem<D>> batch, std::span<std::int32_t> out) override {
+        for (std::size_t i = 0; i < batch.size(); ++i)
+            out[i] = mh_.lookup(batch[i].state);
+        sync_calls_.fetch_add(1);
+    }
+    int max_concurrent_calls() const override { return 4; }
+    int max_in_flight() const override { return lanes_; }
+    void *submit(std::span<const BatchItem<D>> batch) override {
+        const int now_in = in_flight_.fetch_add(1) + 1;
+        int peak = peak_.load();
+        while (now_in > peak && !peak_.compare_exchange_weak(peak, now_in)) {
+        }
+        auto *t = new Token;
+        t->ready_ns = now() + delay_ns_;
+        for (const auto &it : batch)
+            t->vals.push_back(mh_.lookup(it.state));
+        return t;
+    }
+    bool ready(void *token) override { return now() >= static_cast<Token *>(token)->ready_ns; }
+    void complete(void *token, std::span<std::int32_t> out) override {
+        auto *t = static_cast<Token *>(token);
+        while (now() < t->ready_ns)
+            std::this_thread::yield();
+        std::copy(t->vals.begin(), t->vals.end(), out.begin());
+        delete t;
+        in_flight_.fetch_sub(1);
+    }
+    int peak_in_flight() const { return peak_.load(); }
+    int in_flight() const { return in_flight_.load(); }
+    int sync_calls() const { return sync_calls_.load(); }
+
+private:
+    struct Token {
+        std::int64_t ready_ns = 0;
+        std::vector<std::int32_t> vals;
+    };
+    static std::int64_t now() {
+        return std::chrono::duration_cast<std::chrono::nanoseconds>(
+                   std::chrono::steady_clock::now().time_since_epoch())
+            .count();
+    }
+    ManhattanHeuristic<3> mh_;
+    std::int64_t delay_ns_;
+    int lanes_;
+    std::atomic<int> in_flight_{0}, peak_{0}, sync_calls_{0};
+};
+#endif
 void wait_all(const std::vector<Ticket> &ts, double seconds) {
     const auto end = std::chrono::steady_clock::now() + std::chrono::duration<double>(seconds);
     for (const auto &t : ts)
@@ -239,6 +295,70 @@ int main() {
                     CHECK(poll(t) >= 0);
             CHECK(ev.submitted() == ev.resolved());
         }
+    }
+    { // ring only: asynchronous backend, agents pipelining several batches each;
+      // every ticket resolved to its own value once, in-flight batches drained
+      // by close(), never more than the backend's lanes in flight
+        auto be = std::make_unique<AsyncSim>(200);
+        AsyncSim *raw = be.get();
+        Evaluator<D> ev(std::move(be), 16, 0, false, 2, 4);
+        CHECK(ev.in_flight_per_agent() == 4);
+        std::vector<std::thread> th;
+        std::vector<std::vector<std::pair<D::State, Ticket>>> got(6);
+        for (int k = 0; k < 6; ++k)
+            th.emplace_back([&, k] {
+                std::mt19937_64 rng(300 + k);
+                for (int i = 0; i < 5000; ++i) {
+                    const D::State s = walk(rng, 8);
+                    got[k].emplace_back(s, ev.submit(s, {}));
+                }
+            });
+        for (auto &t : th)
+            t.join();
+        ev.close();
+        std::size_t n = 0;
+        for (auto &v : got)
+            for (auto &[s, t] : v) {
+                CHECK(poll(t) == mh.lookup(s));
+                ++n;
+            }
+        CHECK(n == 30000 && ev.resolved() == n && ev.double_resolutions() == 0);
+        CHECK(ev.stats_snapshot().batch_items == n);
+        CHECK(raw->in_flight() == 0 && raw->peak_in_flight() > 1 && raw->peak_in_flight() <= 8);
+    }
+    { // ring only: asynchronous backend under the reference flush policies and
+      // randomized shutdowns (liveness, as the synchronous rounds above)
+        std::mt19937_64 rng(17);
+        for (int round = 0; round < 100; ++round) {
+            const std::size_t B = 1 + rng() % 16;
+            const std::int64_t timeout = static_cast<std::int64_t>(rng() % 3) - 1;
+            Evaluator<D> ev(std::make_unique<AsyncSim>(static_cast<int>(rng() % 50)), B, timeout, false,
+                            1 + static_cast<int>(rng() % 3), 2);
+            std::vector<Ticket> ts;
+            const int count = static_cast<int>(rng() % 60);
+            for (int i = 0; i < count; ++i) {
+                ts.push_back(ev.submit(walk(rng, 6), {}));
+                if (rng() % 8 == 0)
+                    ev.request_flush();
+            }
+            ev.close();
+            for (const auto &t : ts)
+                CHECK(poll(t) >= 0);
+            CHECK(ev.submitted() == ev.resolved());
+            CHECK(ev.double_resolutions() == 0);
+        }
+    }
+    { // ring only: timeout disabled with an async backend: flushes = submissions / capacity
+        const std::size_t B = 16;
+        Evaluator<D> ev(std::make_unique<AsyncSim>(100), B, -1, false, 2, 2);
+        std::mt19937_64 rng(21);
+        std::vector<Ticket> ts;
+        for (std::size_t i = 0; i < 10 * B; ++i)
+            ts.push_back(ev.submit(walk(rng), {}));
+        wait_all(ts, 5);
+        ev.close();
+        const SearchStats st = ev.stats_snapshot();
+        CHECK(st.batches == 10 && st.batch_items == 10 * B && st.max_batch_occupancy == B);
     }
     std::printf("ring evaluator: %s\n", failures ? "FAILED" : "all checks passed");
 #else
