@@ -17,12 +17,12 @@ part 5).  Instances were chosen from the screens in
 profiles/r2_search_screen.jsonl (tests/search_screen.py) among those both sides
 solve in seconds.
 
-Config 1 (BASELINE configs[0]): Korf's 4x4 instance #9
+Config 1 (BASELINE configs[0]): Korf's 4x4 instances #9, #5 and #2
 (proj/data/korf10.txt, committed in tests/golden/instances.npz) with the
 linear-Manhattan model (C = 72, h = Manhattan distance):
 GPU Batch IDA* against the reference's CPU AIDA* with its own
-LinearModelBackend.  Cost 46 and identical thresholds and non-final iteration
-counts (the screen covers #5, #2, #6 and #8 the same way).
+LinearModelBackend.  Costs 46 / 56 / 55 and identical thresholds and
+non-final iteration counts (the d_init sweep covers #6 and #8 the same way).
 """
 from __future__ import annotations
 
@@ -115,17 +115,18 @@ def korf(tmp_path_factory):
     return str(inst), str(w)
 
 
-@pytest.mark.parametrize("index,cost", [(8, 46)])
+@pytest.mark.parametrize("index,cost", [(8, 46), (4, 56), (1, 55)])
 def test_config1_korf_linear_manhattan(korf, index, cost):
-    """Korf #9 here (~10 s a side); #5, #2, #6 and #8 ran the same check in
-    tests/search_screen.py --korf (profiles/r2_search_screen.jsonl, 1-3 min a
-    side).  d_init is fixed on both sides, so the CPU side can run the
-    reference's fastest AIDA* configuration (one subtree per thread)."""
+    """Korf #9, #5 and #2 (a few seconds a side); #6 and #8 ran the same check in
+    tests/korf_dinit_sweep.sh (profiles/r2_korf_dinit.jsonl).  d_init is fixed
+    on both sides (work generation to depth 14, search.hpp:61-79), so the CPU
+    side runs the reference's fastest AIDA* configuration (one subtree per
+    thread) and still expands the same tree."""
     inst, w = korf
     threads = str(len(os.sched_getaffinity(0)))
     common = ["--domain", "stp4", "--instances", inst, "--model", "linear:" + w, "--q", "0.5",
               "--first", str(index), "--count", "1", "--threads", threads, "--time-limit", "600",
-              "--d-init", "12"]
+              "--d-init", "14"]
     g = run(FAST, [*common, "--mode", "gpu", "--work-num", "64", "--batch", "8192", "--timeout-us", "20"],
             {"BIDA_EVAL_AGENTS": "2", "BIDA_EVAL_SHARDS": "16"})
     c = run(REF, [*common, "--mode", "cpu", "--immediate", "--work-num", "1"])
