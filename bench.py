@@ -421,6 +421,62 @@ def search_leg(wl, seconds, threads, impl="fast", gpus=1, evaluators=1, agents=4
     return leg
 
 
+KORF_LEG = (4, 56, 14)  # korf10 index (#5), optimal cost, d_init (profiles/r2_korf_dinit.jsonl)
+
+
+def config1_leg(seconds, threads):
+    """BASELINE configs[0]: Korf's 4x4 #5 (tests/golden/instances.npz, from
+    proj/data/korf10.txt) with the linear-Manhattan model (C = 72) -- the
+    reference's own LinearModelBackend on the GPU (ring evaluator + CB-DFS
+    overlay) and on the CPU (reference AIDA*, one subtree per thread), the same
+    work-generation depth on both sides so the trees are identical."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import paper_2507_11916_b200 as bida
+
+    idx, cost, d_init = KORF_LEG
+    g = np.load(os.path.join(ROOT, "tests", "golden", "instances.npz"))
+    inst, w = f"/tmp/bida_bench_korf_{os.getpid()}.txt", f"/tmp/bida_bench_man4_{os.getpid()}.blin"
+    with open(inst, "w") as f:
+        f.write("".join("stp 4 " + " ".join(str((int(v) >> (4 * c)) & 15) for c in range(16)) + "\n"
+                        for v in g["korf10"]))
+    K, alpha, C = 16, 4.0, 72  # linear-Manhattan weights (SURVEY §8(c)(i))
+    W = np.zeros((1, C, K * K), np.float32)
+    for c in range(C):
+        for cell in range(K):
+            for t in range(K):
+                md = 0 if t == 0 else abs(cell // 4 - t // 4) + abs(cell % 4 - t % 4)
+                W[0, c, cell * K + t] = alpha * c * md - alpha * c * c / (2 * K)
+    with open(w, "wb") as f:
+        f.write(bida.blin1_bytes("stp4", W, C))
+    common = ["--domain", "stp4", "--instances", inst, "--model", "linear:" + w, "--q", "0.5", "--first", str(idx),
+              "--count", "1", "--threads", str(threads), "--d-init", str(d_init), "--time-limit", str(seconds)]
+    out = {}
+    for side, exe, extra, env in (
+            ("gpu", "tools/bin/bida_search_fast", ["--mode", "gpu", "--work-num", "64", "--batch", "8192",
+                                                   "--timeout-us", "20"],
+             {"BIDA_EVAL_AGENTS": "2", "BIDA_EVAL_SHARDS": "16"}),
+            ("cpu_aidastar", "tools/bin/bida_search", ["--mode", "cpu", "--immediate", "--work-num", "1"], {})):
+        r = subprocess.run([os.path.join(ROOT, exe), *common, *extra], capture_output=True, text=True,
+                           timeout=seconds * 3 + 120, env={**os.environ, **env})
+        rows = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+        if r.returncode or not rows:
+            out[side] = {"unavailable": (r.stderr or "no output").strip()[-200:]}
+            continue
+        x = rows[0]
+        out[side] = {"value": x["nodes_per_s"], "unit": "nodes/s", "status": x["status"], "cost": x["cost"],
+                     "time_to_solve_s": x["wall_s"] if x["status"] == "solved" else None,
+                     "generated": x["generated"], "thresholds": x["thresholds"], "mean_batch": x["mean_batch"]}
+    os.unlink(inst)
+    os.unlink(w)
+    g_, c_ = out.get("gpu", {}), out.get("cpu_aidastar", {})
+    same = g_.get("thresholds") is not None and g_.get("thresholds") == c_.get("thresholds")
+    return {"metric": "batch_idastar_nodes_per_s", "instance": f"korf10 #{idx + 1} (optimal cost {cost})",
+            "model": "linear-Manhattan BLIN1, C=72 (LinearModelBackend)", "d_init": d_init, "threads": threads,
+            **out, "same_thresholds": same,
+            "cpu_baseline": {"value": c_.get("value"), "unit": "nodes/s", "cores": threads, "kind": "reference",
+                             "sample": "the same search, reference AIDA* (immediate LinearModelBackend)"}}
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -711,6 +767,9 @@ def main():
                     if cp and "value" in cp:
                         sr["cpu_pdb_only"] = cp
             line["search"] = sr
+            if world == 1:
+                line["search_config1"] = config1_leg(min(args.search_seconds, 60.0), threads)
+                mark("search_config1")
     line["bench_seconds"] = timings
     print(json.dumps(line), flush=True)
 
