@@ -110,7 +110,7 @@ inline int default_shards() {
     const int k = s ? std::atoi(s) : 8;
     return std::clamp(k, 1, 64);
 }
-inline int env_inflight() {  // BIDA_EVAL_INFLIGHT: batches in flight per agent (0 = backend's share)
+inline int env_inflight() {  // BIDA_EVAL_INFLIGHT: batches in flight per agent (default 1: synchronous)
     const char *s = std::getenv("BIDA_EVAL_INFLIGHT");
     return s ? std::clamp(std::atoi(s), 0, 64) : 0;
 }
@@ -164,11 +164,14 @@ public:
             // in-flight batches per agent: the backend's lanes shared by the
             // agents (so an agent blocked in submit() never waits on lanes only
             // blocked agents hold); 1 = synchronous evaluate()
+            // Opt-in (BIDA_EVAL_INFLIGHT=d > 1): measured on one B200 the search is
+            // bound by the agents' per-item host work, not by round trips in
+            // flight (profiles/r2_search_async_sweep.jsonl), so the default stays
+            // one synchronous call per agent.
             async_ = dynamic_cast<AsyncEvaluatorBackend<D> *>(backend_.get());
             if (async_) {
                 const int env = ring_detail::env_inflight();
-                depth_ = env > 0 ? env : std::max(1, async_->max_in_flight() / k_agents);
-                depth_ = std::min(depth_, std::max(1, async_->max_in_flight() / k_agents));
+                depth_ = std::min(env, std::max(1, async_->max_in_flight() / k_agents));
                 if (depth_ <= 1)
                     async_ = nullptr;
             }
@@ -345,8 +348,13 @@ private:
         epoch_.notify_all();
     }
 
+    // A slot is resolved only by the agent that claimed it, so a load + release
+    // store replaces the reference's exchange (batch_eval.hpp:302-306; one
+    // locked instruction per node less) and still counts a second resolution.
     void resolve(TicketSlot &t, std::int32_t v) {
-        if (t.value.exchange(v, std::memory_order_release) != -1)
+        const std::int32_t prev = t.value.load(std::memory_order_relaxed);
+        t.value.store(v, std::memory_order_release);
+        if (prev != -1)
             double_resolved_.fetch_add(1, std::memory_order_relaxed);
     }
 

@@ -8,6 +8,7 @@
 #include <array>
 #include <atomic>
 #include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <random>
 #include <thread>
@@ -299,6 +300,7 @@ int main() {
     { // ring only: asynchronous backend, agents pipelining several batches each;
       // every ticket resolved to its own value once, in-flight batches drained
       // by close(), never more than the backend's lanes in flight
+        setenv("BIDA_EVAL_INFLIGHT", "4", 1);
         auto be = std::make_unique<AsyncSim>(200);
         AsyncSim *raw = be.get();
         Evaluator<D> ev(std::move(be), 16, 0, false, 2, 4);
