@@ -172,8 +172,10 @@ public:
             if (async_) {
                 const int env = ring_detail::env_inflight();
                 depth_ = std::min(env, std::max(1, async_->max_in_flight() / k_agents));
-                if (depth_ <= 1)
+                if (depth_ <= 1) {
                     async_ = nullptr;
+                    depth_ = 1;
+                }
             }
             for (int k = 0; k < k_agents; ++k)
                 agents_.emplace_back([this] { agent_loop(); });
@@ -391,7 +393,7 @@ private:
             // completed device batches first (resolves their tickets)
             while (!inflight.empty() && async_->ready(inflight.front().token))
                 finish_front();
-            if (inflight.size() >= static_cast<std::size_t>(depth_)) {
+            if (!inflight.empty() && inflight.size() >= static_cast<std::size_t>(depth_)) {
                 finish_front();  // pipeline full: wait for the oldest
                 continue;
             }

@@ -300,6 +300,24 @@ int main() {
     { // ring only: asynchronous backend, agents pipelining several batches each;
       // every ticket resolved to its own value once, in-flight batches drained
       // by close(), never more than the backend's lanes in flight
+        // an async-capable backend with BIDA_EVAL_INFLIGHT unset: synchronous calls
+        unsetenv("BIDA_EVAL_INFLIGHT");
+        {
+            auto sb = std::make_unique<AsyncSim>(50);
+            AsyncSim *sraw = sb.get();
+            Evaluator<D> sev(std::move(sb), 16, 0, false, 2, 4);
+            CHECK(sev.in_flight_per_agent() == 1);
+            std::mt19937_64 srng(301);
+            std::vector<std::pair<D::State, Ticket>> sv;
+            for (int i = 0; i < 3000; ++i) {
+                const D::State s = walk(srng, 8);
+                sv.emplace_back(s, sev.submit(s, {}));
+            }
+            sev.close();
+            for (auto &[s, t] : sv)
+                CHECK(poll(t) == mh.lookup(s));
+            CHECK(sraw->peak_in_flight() == 0 && sraw->sync_calls() > 0);
+        }
         setenv("BIDA_EVAL_INFLIGHT", "4", 1);
         auto be = std::make_unique<AsyncSim>(200);
         AsyncSim *raw = be.get();
