@@ -1,8 +1,3 @@
 cd "$(dirname "$0")"
-rm -f gpurun_out/host_sweep.jsonl
-timeout 900 python bench.py > gpurun_out/r2_bench4.json 2> gpurun_out/r2_bench4.err
-for th in 12 16; do for ag in 4; do
-  BIDA_EVAL_AGENTS=$ag BIDA_EVAL_SHARDS=16 timeout 200 tools/bin/bida_search_fast --domain rc --walks 1:14:14:2508 \
-    --model mlp:/tmp/h128.bmlp --q 0.5 --table1-pdb 8 --pdb-build gpu --threads $th --mode gpu --gpu-pdb \
-    --work-num 128 --batch 16384 --timeout-us 25 --time-limit 120 | python -c "import json,sys; r=json.loads(sys.stdin.readline()); r.update(agents=$ag); print(json.dumps({k:r[k] for k in ['status','cost','generated','wall_s','nodes_per_s','mean_batch','threads','agents']}))" >> gpurun_out/host_sweep.jsonl
-done; done
+timeout 900 python -m pytest tests/test_gpu_mlp.py tests/test_gpu_linear.py tests/test_gpu_parity_scale.py -x -q > gpurun_out/r2_t7.log 2>&1
+for w in rc-mlp-h128 rc-mlp-h256 rc-linear-e1-c21; do timeout 300 python bench.py --workload $w --steps 20 --warmup 5 --no-cpu-baseline --search-seconds 0 --no-wide-leg --no-linear-leg --no-sweep 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print(json.dumps({'workload':'$w','value':d['value'],'frac':d['roofline']['frac'],'e2e':d['e2e']['value']}))" >> gpurun_out/r2_quick_bench.jsonl; done
