@@ -86,7 +86,7 @@ def lib() -> C.CDLL:
             f"CUDA evaluator library not built: {LIB_PATH} is missing "
             "(run `python -c 'import __graft_entry__ as g; g.build()'`)"
         )
-    path = LIB_PATH
+    path = os.environ.get("BIDA_GPU_LIB") or LIB_PATH  # A/B benchmarking of another build
     if os.environ.get("BIDA_GPU_TRACE") == "1":  # diagnostic build with the kernel timeline compiled in
         path = os.path.join(HERE, "_lib", "libbida_gpu_trace.so")
     L = C.CDLL(path)
