@@ -536,6 +536,24 @@ def cpu_baseline_and_parity(args, wl, timed_batch, local):
     return cpu, parity
 
 
+def pcie_h2d_gbs(local, nbytes=1 << 28, reps=5):
+    """Measured host->device copy bandwidth from page-locked memory (the link
+    the end-to-end path streams packed states over), best of `reps`."""
+    import torch
+
+    src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", local))
+    best = 0.0
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, nbytes / (a.elapsed_time(b) * 1e-3) / 1e9)
+    return best
+
+
 def batch_sweep(wl, local, sizes=None):
     """BASELINE configs[2]: evals/s vs batch size 2^10..2^20 on one GPU, device-
     resident (CUDA events over R back-to-back launches on the launching
@@ -702,6 +720,12 @@ def main():
         "clocks": r["clocks"],
         "kernel_ms_avg": r["kern_avg_ms"],
     }
+    if world == 1:
+        # the end-to-end path's own roofline: packed states over PCIe, host -> device
+        h2d = pcie_h2d_gbs(local)
+        got = line["e2e"]["value"] * PACKED[wl["domain"]] / 1e9
+        line["e2e"]["pcie"] = {"h2d_gbs_measured": h2d, "h2d_gbs_achieved": got, "frac": got / h2d,
+                               "how": "pinned 256 MB torch copy_, best of 5, CUDA events"}
     if world == 1 and args.wide_leg and args.workload != WIDE_WORKLOAD:
         # config 4 (the paper's 13.6 MB model): the tensor-bound case
         # the north star's tensor-utilisation target refers to; device-resident only

@@ -170,31 +170,30 @@ int launch_linear_d(bida_gpu_evaluator *ev, const LinearArgs &a, cudaStream_t st
 }
 
 // Thread-per-state linear kernel (linear_thread.cuh): one instantiation per
-// (domain, class-slot count, weights staged in shared memory or not).
+// (domain, class-slot count).
 template <int DOMAIN, int CM>
-void *linear_thread_fn(bool smem) {
-    return smem ? reinterpret_cast<void *>(linear_thread_kernel<DOMAIN, CM, true>)
-                : reinterpret_cast<void *>(linear_thread_kernel<DOMAIN, CM, false>);
+void *linear_thread_fn() {
+    return reinterpret_cast<void *>(linear_thread_kernel<DOMAIN, CM>);
 }
 
 template <int DOMAIN>
-void *linear_thread_fn_cm(int cm, bool smem) {
+void *linear_thread_fn_cm(int cm) {
     switch (cm) {
-    case 8: return linear_thread_fn<DOMAIN, 8>(smem);
-    case 16: return linear_thread_fn<DOMAIN, 16>(smem);
-    case 24: return linear_thread_fn<DOMAIN, 24>(smem);
-    case 32: return linear_thread_fn<DOMAIN, 32>(smem);
-    case 64: return linear_thread_fn<DOMAIN, 64>(smem);
-    default: return linear_thread_fn<DOMAIN, 96>(smem);
+    case 8: return linear_thread_fn<DOMAIN, 8>();
+    case 16: return linear_thread_fn<DOMAIN, 16>();
+    case 24: return linear_thread_fn<DOMAIN, 24>();
+    case 32: return linear_thread_fn<DOMAIN, 32>();
+    case 64: return linear_thread_fn<DOMAIN, 64>();
+    default: return linear_thread_fn<DOMAIN, 96>();
     }
 }
 
-void *linear_thread_kernel_for(int domain, int cm, bool smem) {
+void *linear_thread_kernel_for(int domain, int cm) {
     switch (domain) {
-    case BIDA_DOMAIN_STP2: return linear_thread_fn_cm<kSTP2>(cm, smem);
-    case BIDA_DOMAIN_STP3: return linear_thread_fn_cm<kSTP3>(cm, smem);
-    case BIDA_DOMAIN_STP4: return linear_thread_fn_cm<kSTP4>(cm, smem);
-    default: return linear_thread_fn_cm<kRC>(cm, smem);
+    case BIDA_DOMAIN_STP2: return linear_thread_fn_cm<kSTP2>(cm);
+    case BIDA_DOMAIN_STP3: return linear_thread_fn_cm<kSTP3>(cm);
+    case BIDA_DOMAIN_STP4: return linear_thread_fn_cm<kSTP4>(cm);
+    default: return linear_thread_fn_cm<kRC>(cm);
     }
 }
 
@@ -214,7 +213,8 @@ int launch_linear_thread(bida_gpu_evaluator *ev, const void *d_packed, int64_t n
     a.rk.uHi = ev->uHi;
     // small batches (the search's zero-copy regime) read the weights through
     // L1/L2 instead of staging the whole table into every CTA's shared memory
-    const bool smem = ev->w_in_smem && n > kLinSmallBatch;
+    const bool small = n <= kLinSmallBatch;
+    a.w_in_smem = small ? 0 : ev->w_in_smem;
     a.err = err;
     a.replays = ev->d_replays;
     a.pdb = ev->pdb;
@@ -223,8 +223,8 @@ int launch_linear_thread(bida_gpu_evaluator *ev, const void *d_packed, int64_t n
     const int64_t want = (n + kLinThreads - 1) / kLinThreads;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, ev->lin_grid_cap)));
     void *args[] = {&a};
-    CUDA_TRY(cudaLaunchKernel(linear_thread_kernel_for(ev->domain, ev->lin_cm, smem), dim3(grid), dim3(kLinThreads),
-                              args, smem ? ev->lin_smem : 0, st));
+    CUDA_TRY(cudaLaunchKernel(linear_thread_kernel_for(ev->domain, ev->lin_cm), dim3(grid), dim3(kLinThreads),
+                              args, small ? 0 : ev->lin_smem, st));
     ev->launches.fetch_add(1, std::memory_order_relaxed);
     return BIDA_OK;
 }
@@ -531,8 +531,8 @@ int linear_create_impl(int device, int domain, const float *weights, int E, int 
         const size_t wbytes = w3.size() * sizeof(float);
         ev->w_in_smem = wbytes <= 200 * 1024 ? 1 : 0;
         ev->lin_smem = ev->w_in_smem ? wbytes : 0;
-        void *fn = linear_thread_kernel_for(domain, ev->lin_cm, ev->w_in_smem != 0);
-        if (ev->w_in_smem && ev->lin_smem > 48 * 1024) {
+        void *fn = linear_thread_kernel_for(domain, ev->lin_cm);
+        if (ev->lin_smem > 48 * 1024) {
             e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ev->lin_smem));
             if (e != cudaSuccess)
                 return bail(fail(BIDA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e)));

@@ -197,6 +197,7 @@ struct LinearThreadArgs {
     const float *W;          // global [E][F+1][Cp]
     int E, C, Cp;
     ReadoutConsts rk;
+    int w_in_smem;
     int *err;
     unsigned long long *replays;  // optional: readouts that took the exact replay
     PdbArgs pdb;
@@ -205,9 +206,7 @@ struct LinearThreadArgs {
 // CM: class slots (multiple of 4, >= C).  CM <= 32: the float64 logits stay in
 // registers; CM > 32: pass 1 finds the float64 maximum, pass 2 recomputes each
 // logit and keeps only fl32(l - max) (the register budget of 96 doubles).
-// SMEM: the weight table is staged in shared memory (one instantiation each, so
-// the row loads compile to LDS.128 / LDG.128 instead of generic LD.E.128).
-template <int DOMAIN, int CM, bool SMEM>
+template <int DOMAIN, int CM>
 __global__ void __launch_bounds__(kLinThreads, CM <= 32 ? 2 : 1)
 linear_thread_kernel(const LinearThreadArgs a) {
     using T = DomainTraits<DOMAIN>;
@@ -216,8 +215,8 @@ linear_thread_kernel(const LinearThreadArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int C = a.C, Cp = a.Cp, E = a.E;
     const size_t per_member = static_cast<size_t>(F + 1) * Cp;
-    const float *W;
-    if constexpr (SMEM) {
+    const float *W = a.W;
+    if (a.w_in_smem) {
         float4 *dst = reinterpret_cast<float4 *>(smem);
         const float4 *src = reinterpret_cast<const float4 *>(a.W);
         const size_t n4 = per_member * E / 4;
@@ -225,8 +224,6 @@ linear_thread_kernel(const LinearThreadArgs a) {
             dst[i] = __ldg(src + i);
         __syncthreads();
         W = reinterpret_cast<const float *>(smem);
-    } else {
-        W = a.W;
     }
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < a.n; s += stride) {

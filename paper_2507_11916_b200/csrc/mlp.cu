@@ -88,8 +88,7 @@ struct MlpParams {
     uint8_t *scratch;   // wide: per-CTA hidden activations, 2 buffers of sbytes (global, L2-resident)
     long long sbytes;
     int stage_bytes;    // wide: bytes per weight/activation stage
-    int bias_bytes;     // whole bias vector staged in shared memory (0: read from global)
-    int bias_soff;      // fused schedules: its shared-memory offset
+    int bias_bytes;     // wide: whole bias vector staged in shared memory (0: read from global)
     int l2hint;         // wide: evict_last L2 policy on scratch stores and stage copies
 };
 
@@ -202,7 +201,7 @@ __device__ __forceinline__ void requant_block(uint32_t t_row, int t0, const int3
 // bias): the TMEM load of the next 16 columns is in flight while the current
 // 16 are requantised and stored.  Columns [c_beg, c_end) of this thread's row.
 __device__ __forceinline__ void requant_pipelined(uint32_t t_row, const int32_t *bias, int sh, uint32_t out, int row,
-                                                  int c_beg, int c_end, uint32_t bias_s = 0u) {
+                                                  int c_beg, int c_end) {
     auto requant = [&](const int32_t(&r)[16], const int4(&b4)[4], int c0) {
         uint32_t w[4];
 #pragma unroll
@@ -214,8 +213,7 @@ __device__ __forceinline__ void requant_pipelined(uint32_t t_row, const int32_t 
     auto load_bias = [&](int4(&b4)[4], int c0) {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            b4[q] = bias_s ? sm100::ld_shared_v4(bias_s + (c0 + 4 * q) * 4u)
-                           : __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
+            b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
     };
     int32_t ra[16], rb[16];
     int4 ba[4], bb[4];
@@ -299,12 +297,6 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
     }
     if (warp == 1)
         sm100::tmem_alloc(tmem_slot, p.tmem_cols);
-    // all biases staged in shared memory once per CTA (the epilogue's per-column
-    // __ldg of them was a long-scoreboard stall, profiles/r2_h128.txt)
-    const uint32_t bias_s = p.bias_bytes ? sm100::smem_u32(smem + p.bias_soff) : 0u;
-    if (p.bias_bytes)
-        for (int i = threadIdx.x; i < p.bias_bytes / 16; i += blockDim.x)
-            reinterpret_cast<int4 *>(smem + p.bias_soff)[i] = __ldg(reinterpret_cast<const int4 *>(p.bias) + i);
     sm100::tc_fence_before();
     __syncthreads();
     if (mc)
@@ -609,8 +601,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                         const uint32_t out = ((l + 1) & 1) ? sY : sX;
                         const int half = mode == kPair ? ly.N : ly.N / 2;
                         const int c_beg = mode == kPair ? 0 : grp * half, c_end = c_beg + half;
-                        requant_pipelined(t_row, bias, ly.shift, out, row, c_beg, c_end,
-                                          bias_s ? bias_s + ly.boff * 4u : 0u);
+                        requant_pipelined(t_row, bias, ly.shift, out, row, c_beg, c_end);
                         sm100::tc_fence_before();
                         sm100::fence_proxy_async_smem();
                         tr(70 + l);
@@ -627,8 +618,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                     int4 b4[4];
 #pragma unroll
                                     for (int q = 0; q < 4; ++q)
-                                        b4[q] = bias_s ? sm100::ld_shared_v4(bias_s + (ly.boff + c0 + 4 * q) * 4u)
-                                                       : __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
+                                        b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
                                     sm100::tmem_wait_ld();
 #pragma unroll
                                     for (int q = 0; q < 4; ++q) {
@@ -1410,18 +1400,6 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     } else {
         delete m;
         return fail(err, 1, "BMLP1: model too wide for shared memory");
-    }
-    if (p.mode != kWide) {
-        // fused schedules: the whole bias vector behind everything else, if it fits
-        const size_t bb = bias.size() * 4;  // N padded to 16: a multiple of 64 bytes
-        const size_t off = (m->smem + 15) & ~size_t(15);
-        if (off + bb <= budget) {
-            p.bias_soff = static_cast<int>(off);
-            p.bias_bytes = static_cast<int>(bb);
-            m->smem = off + bb;
-        } else {
-            p.bias_bytes = 0;
-        }
     }
     // Weight image, per layer in MMA consumption order: nh N-halves (2 for the
     // split schedule's hidden layers, else 1), each K/32 chunks of
