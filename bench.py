@@ -763,20 +763,21 @@ def main():
         # Batch IDA* nodes/s on all `world` GPUs from one host process (rank 0; one
         # evaluator per GPU, tid % E routing, batch_eval.hpp:398-400)
         threads = host_cores()
-        # host-core budget (profiles/r2_search_host_sweep.jsonl): 4 agent threads per
-        # GPU evaluator, searcher threads on the remaining cores
-        gpu_threads = max(threads // 2, threads - 4 * world)
+        # host-core budget (profiles/r2_search_host_sweep.jsonl): up to 4 agent threads
+        # per GPU evaluator within half the cores, searcher threads on the rest
+        agents = max(1, min(4, (threads // 2) // world))
+        gpu_threads = max(threads // 2, threads - agents * world)
         plan = search_plan(rank, world)
-        sr = search_leg(wl, args.search_seconds, gpu_threads, **plan)
+        sr = search_leg(wl, args.search_seconds, gpu_threads, agents=agents, **plan)
         mark("search_" + plan["impl"])
         if sr is not None:
             sr = {"metric": "batch_idastar_nodes_per_s", **sr,
                   "config": {"domain": "rc", "heuristic": "BMLP1 evaluated per node + 8-corner PDB guidance "
                              "(PAPER.md:407 Table-1 mode)", "search": "reference batch_idastar (search.hpp:101-237)",
-                             "host": f"{gpu_threads} searcher threads + 4 agent threads per GPU on {threads} host cores"}}
+                             "host": f"{gpu_threads} searcher threads + {agents} agent threads per GPU on {threads} host cores"}}
             if world == 1:
                 legs = {}
-                for impl, kw in (("ring", {}), ("reference", {"evaluators": 8, "agents": 1})):
+                for impl, kw in (("ring", {"agents": agents}), ("reference", {"evaluators": 8, "agents": 1})):
                     r2 = search_leg(wl, args.search_seconds, gpu_threads, impl=impl, **kw)
                     if r2 is not None:
                         legs[impl] = r2
