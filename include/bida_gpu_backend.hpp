@@ -43,6 +43,37 @@
 
 namespace bida_gpu {
 
+// Packing the agent does for every state of every batch (the wire format is
+// exactly D::pack's).  With BMI2 (checked at run time) each byte-array field is
+// gathered by one PEXT instead of a shift-or per element; a state with a byte
+// outside its field's range (never produced by the search) takes D::pack, whose
+// OR of overlapping fields the masked gather would not reproduce.
+namespace pack_detail {
+inline bool has_bmi2() {
+#if defined(__x86_64__)
+    static const bool yes = __builtin_cpu_supports("bmi2");
+    return yes;
+#else
+    return false;
+#endif
+}
+inline std::uint64_t rd64(const std::uint8_t *p) {
+    std::uint64_t v;
+    std::memcpy(&v, p, 8);
+    return v;
+}
+inline std::uint32_t rd32(const std::uint8_t *p) {
+    std::uint32_t v;
+    std::memcpy(&v, p, 4);
+    return v;
+}
+#if defined(__x86_64__)
+__attribute__((target("bmi2"))) inline std::uint64_t pext(std::uint64_t v, std::uint64_t m) {
+    return __builtin_ia32_pext_di(v, m);
+}
+#endif
+}  // namespace pack_detail
+
 template <class D>
 struct DomainOf;
 template <int N>
@@ -50,6 +81,19 @@ struct DomainOf<bida::TilePuzzle<N>> {
     static constexpr int id = N;  // BIDA_DOMAIN_STP2..4
     static constexpr int packed_bytes = 8;
     static void pack(const typename bida::TilePuzzle<N>::State &s, unsigned char *out) {
+#if defined(__x86_64__)
+        if constexpr (N == 4) {
+            if (pack_detail::has_bmi2()) {
+                const std::uint64_t a = pack_detail::rd64(s.tiles.data()), b = pack_detail::rd64(s.tiles.data() + 8);
+                if (((a | b) & 0xF0F0F0F0F0F0F0F0ull) == 0) {
+                    const std::uint64_t v = pack_detail::pext(a, 0x0F0F0F0F0F0F0F0Full) |
+                                            pack_detail::pext(b, 0x0F0F0F0F0F0F0F0Full) << 32;
+                    std::memcpy(out, &v, 8);
+                    return;
+                }
+            }
+        }
+#endif
         const std::uint64_t v = bida::TilePuzzle<N>::pack(s);  // stp.hpp:121-126
         std::memcpy(out, &v, 8);
     }
@@ -59,6 +103,25 @@ struct DomainOf<bida::RubiksCube> {
     static constexpr int id = BIDA_DOMAIN_RC;
     static constexpr int packed_bytes = 16;
     static void pack(const bida::RubiksCube::State &s, unsigned char *out) {
+#if defined(__x86_64__)
+        if (pack_detail::has_bmi2()) {
+            using namespace pack_detail;
+            const std::uint64_t cp = rd64(s.cp.data()), co = rd64(s.co.data());
+            const std::uint64_t ep0 = rd64(s.ep.data()), eo0 = rd64(s.eo.data());
+            const std::uint32_t ep1 = rd32(s.ep.data() + 8), eo1 = rd32(s.eo.data() + 8);
+            const bool in_range = (cp & 0xF8F8F8F8F8F8F8F8ull) == 0 && (co & 0xFCFCFCFCFCFCFCFCull) == 0 &&
+                                  (eo0 & 0xFEFEFEFEFEFEFEFEull) == 0 && (eo1 & 0xFEFEFEFEu) == 0 &&
+                                  (ep0 & 0xF0F0F0F0F0F0F0F0ull) == 0 && (ep1 & 0xF0F0F0F0u) == 0;
+            if (in_range) {
+                const std::uint64_t lo = pext(cp, 0x0707070707070707ull) | pext(co, 0x0303030303030303ull) << 24 |
+                                         pext(eo0, 0x0101010101010101ull) << 40 | pext(eo1, 0x01010101ull) << 48;
+                const std::uint64_t hi = pext(ep0, 0x0F0F0F0F0F0F0F0Full) | pext(ep1, 0x0F0F0F0Full) << 32;
+                std::memcpy(out, &lo, 8);
+                std::memcpy(out + 8, &hi, 8);
+                return;
+            }
+        }
+#endif
         const bida::RubiksCube::Packed p = bida::RubiksCube::pack(s);  // rubiks.hpp:126-137
         std::memcpy(out, &p.lo, 8);
         std::memcpy(out + 8, &p.hi, 8);

@@ -190,3 +190,13 @@ def test_fast_cbdfs_rc_pdb_multi_evaluator():
     assert [r["status"] for r in fast] == ["solved"] * 3
     assert [r["cost"] for r in fast] == [r["cost"] for r in ref]
     assert [r["thresholds"] for r in fast] == [r["thresholds"] for r in ref]
+
+
+def test_fast_pack_matches_reference_pack():
+    """The agent's PEXT state packing (include/bida_gpu_backend.hpp) equals the
+    reference's D::pack on 4 M random in- and out-of-range states."""
+    exe = os.path.join(ROOT, "tests", "cpp", "bin", "pack_check")
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
