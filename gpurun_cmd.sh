@@ -1,5 +1,5 @@
 cd "$(dirname "$0")"
-rm -f gpurun_out/search_configs.jsonl gpurun_out/parity_scale.jsonl gpurun_out/pdb_build.jsonl
-timeout 900 python bench.py > gpurun_out/r2_bench5.json 2> gpurun_out/r2_bench5.err
-timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/r2_gputests_full2.log 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke.log 2>&1
+rm -f gpurun_out/search_ab.jsonl
+bash tests/search_ab.sh bida_search_fast_prev bida_search_fast 3 > gpurun_out/search_ab.log 2>&1
+python bench.py --steps 3 --warmup 3 --no-cpu-baseline --search-seconds 0 --no-wide-leg --no-linear-leg --no-sweep > gpurun_out/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_launches_default.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --search-seconds 0 --no-wide-leg --no-linear-leg --no-sweep > gpurun_out/ncu_launch.log 2>&1

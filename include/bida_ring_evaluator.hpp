@@ -30,9 +30,10 @@
 // items per backend call, evaluate_single / evaluate_sync on the caller
 // thread, immediate mode, stats (one record_batch per backend batch,
 // forced_flushes, sync_evaluations), submission after close throws
-// std::runtime_error.  The only policy difference: after a full batch is
-// taken from a longer queue the reference restarts the timeout clock at
-// "now", this ring uses the next item's own submit time (flushes no later).
+// std::runtime_error.  Timeout clock: the oldest pending item's age counts
+// from its submission when it was its shard's head then, else from when an
+// agent first saw it as the head -- as the reference restarts its clock at
+// "now" after taking a full batch from a longer queue.
 //
 // Used by building the reference's search against include/overlay/ (see
 // tools/Makefile: bida_search_ring), where bida/batch_eval.hpp is the
@@ -292,7 +293,7 @@ public:
 private:
     struct Meta {
         std::atomic<std::uint64_t> seq{0}; // == pos: free for lap pos; == pos+1: published
-        std::int64_t t_ns = 0;             // submit time (timeout > 0 only)
+        std::int64_t t_ns = 0;             // timeout > 0: time this item became its shard's head (0: not yet)
         TicketSlot *raw = nullptr;         // submit_slot(): resolve here instead of the item's ticket
     };
     struct Shard {
@@ -329,8 +330,13 @@ private:
         it.state = state;
         it.features = std::move(features);
         m.raw = raw;
+        // only the oldest pending item's age matters (the flush deadline): an
+        // item stamps its submit time when it is its shard's head; an item
+        // queued behind others is stamped by the agent when it becomes the
+        // head (as the reference restarts its clock after a full batch), which
+        // keeps a clock read off almost every submit
         if (timeout_us_ > 0)
-            m.t_ns = ring_detail::now_ns();
+            m.t_ns = sh.head.load(std::memory_order_relaxed) == pos ? ring_detail::now_ns() : 0;
         m.seq.store(pos + 1, std::memory_order_seq_cst);
         sh.inflight.fetch_sub(1, std::memory_order_release);
         const std::uint64_t depth = pos + 1 - sh.head.load(std::memory_order_seq_cst);
@@ -417,8 +423,12 @@ private:
                 if (c) {
                     ranges.push_back({k, h, c});
                     n += c;
-                    if (timeout_us_ > 0)
-                        oldest = std::min(oldest, sh.meta[h & mask_].t_ns);
+                    if (timeout_us_ > 0) {
+                        Meta &hm = sh.meta[h & mask_];  // published: its producer is done with it
+                        if (hm.t_ns == 0)
+                            hm.t_ns = ring_detail::now_ns();
+                        oldest = std::min(oldest, hm.t_ns);
+                    }
                 }
             }
             const bool closed = closed_.load(std::memory_order_acquire);
