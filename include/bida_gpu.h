@@ -122,6 +122,12 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
  * a ninth submit waits for a lane. */
 typedef struct bida_gpu_batch bida_gpu_batch;
 int bida_gpu_submit(bida_gpu_evaluator *ev, const void *packed, int64_t n, bida_gpu_batch **out);
+/* The same in two steps, without the staging copy: bida_gpu_batch_begin
+ * reserves a lane for n <= 32768 states and returns its mapped (write-combined)
+ * host input buffer; the caller packs the states straight into it, then
+ * bida_gpu_batch_launch starts the evaluation (ready / h / wait as above). */
+int bida_gpu_batch_begin(bida_gpu_evaluator *ev, int64_t n, bida_gpu_batch **out, void **in_host);
+int bida_gpu_batch_launch(bida_gpu_batch *b);
 int bida_gpu_batch_ready(bida_gpu_batch *b);
 const int32_t *bida_gpu_batch_h(bida_gpu_batch *b);
 int bida_gpu_batch_wait(bida_gpu_batch *b, int32_t *h_out);

@@ -232,8 +232,29 @@ public:
 #endif
 
     void evaluate(std::span<const bida::BatchItem<D>> batch, std::span<std::int32_t> out) override {
-        thread_local std::vector<unsigned char> staging;
         const std::size_t n = batch.size();
+        if (n > 0 && n <= 32768) {
+            // pack straight into a zero-copy lane's mapped input (no staging copy)
+            bida_gpu_batch *b = nullptr;
+            void *in = nullptr;
+            if (bida_gpu_batch_begin(handle_, static_cast<std::int64_t>(n), &b, &in) == BIDA_OK) {
+                auto *dst = static_cast<unsigned char *>(in);
+                for (std::size_t i = 0; i < n; ++i)
+                    Traits::pack(batch[i].state, dst + i * Traits::packed_bytes);
+                int rc = bida_gpu_batch_launch(b);
+                if (rc == BIDA_OK)
+                    rc = bida_gpu_batch_wait(b, out.data());  // zero-fills out on error
+                calls_.fetch_add(1, std::memory_order_relaxed);
+                items_.fetch_add(n, std::memory_order_relaxed);
+                if (rc) {
+                    for (auto &v : out)
+                        v = 0;
+                    note_error();
+                }
+                return;
+            }
+        }
+        thread_local std::vector<unsigned char> staging;
         staging.resize(n * Traits::packed_bytes);
         for (std::size_t i = 0; i < n; ++i)
             Traits::pack(batch[i].state, staging.data() + i * Traits::packed_bytes);

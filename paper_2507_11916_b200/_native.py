@@ -55,6 +55,8 @@ EXPORTS = [
     "bida_gpu_evaluate_logits",
     "bida_gpu_evaluate_device",
     "bida_gpu_submit",
+    "bida_gpu_batch_begin",
+    "bida_gpu_batch_launch",
     "bida_gpu_batch_ready",
     "bida_gpu_batch_h",
     "bida_gpu_batch_wait",
@@ -107,6 +109,8 @@ def lib() -> C.CDLL:
     L.bida_gpu_evaluate_device.argtypes = [H, vp, i64, vp, vp, vp]
     L.bida_gpu_stream_status.argtypes = [H]
     L.bida_gpu_submit.argtypes = [H, vp, i64, C.POINTER(vp)]
+    L.bida_gpu_batch_begin.argtypes = [H, i64, C.POINTER(vp), C.POINTER(vp)]
+    L.bida_gpu_batch_launch.argtypes = [vp]
     L.bida_gpu_batch_ready.argtypes = [vp]
     L.bida_gpu_batch_h.argtypes = [vp]
     L.bida_gpu_batch_h.restype = C.POINTER(C.c_int32)

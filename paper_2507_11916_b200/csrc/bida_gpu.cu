@@ -844,6 +844,51 @@ int bida_gpu_evaluate(bida_gpu_evaluator *ev, const void *packed, int64_t n, int
     return bida_gpu_evaluate_logits(ev, packed, n, h_out, nullptr);
 }
 
+int bida_gpu_batch_begin(bida_gpu_evaluator *ev, int64_t n, bida_gpu_batch **out, void **in_host) {
+    if (!out || !in_host)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "out pointers are NULL");
+    *out = nullptr;
+    *in_host = nullptr;
+    if (!ev)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL evaluator");
+    if (n < 0)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "bad batch arguments");
+    if (n > kZeroCopyMax)
+        return fail(BIDA_ERR_CAPACITY, "asynchronous batches hold at most 32768 states");
+    bida_gpu_evaluator::ZcLane *ln = acquire_lane(ev);
+    ln->n = n;
+    *out = reinterpret_cast<bida_gpu_batch *>(ln);
+    *in_host = ln->in;
+    return BIDA_OK;
+}
+
+int bida_gpu_batch_launch(bida_gpu_batch *b) {
+    if (!b)
+        return fail(BIDA_ERR_INVALID_ARGUMENT, "NULL batch");
+    auto *ln = reinterpret_cast<bida_gpu_evaluator::ZcLane *>(b);
+    bida_gpu_evaluator *ev = ln->owner;
+    const int ch = static_cast<int>(ln - ev->zc);
+    int rc = BIDA_OK;
+    cudaError_t e = cudaSetDevice(ev->device);
+    if (e != cudaSuccess)
+        rc = fail(BIDA_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+    if (rc == BIDA_OK)
+        rc = launch(ev, ln->in_dev, ln->n, ln->out_dev, nullptr, ln->st, chan_err(ev, ch));
+    if (rc == BIDA_OK) {
+        e = cudaEventRecord(ln->done, ln->st);
+        if (e != cudaSuccess)
+            rc = fail(BIDA_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+    }
+    if (rc != BIDA_OK) {
+        cudaStreamSynchronize(ln->st);
+        collect_errors(ev, ch);
+        release_lane(ln);
+        return rc;
+    }
+    ev->zc_calls.fetch_add(1, std::memory_order_relaxed);
+    return BIDA_OK;
+}
+
 int bida_gpu_submit(bida_gpu_evaluator *ev, const void *packed, int64_t n, bida_gpu_batch **out) {
     NvtxRange nvtx("bida_gpu_submit");
     if (!out)

@@ -74,3 +74,23 @@ def test_async_from_many_threads():
         for th in ths:
             th.join()
     assert not errors
+
+
+def test_begin_fill_launch_wait():
+    """bida_gpu_batch_begin hands out the lane's mapped input buffer; the caller
+    packs states straight into it (GpuBackend does), launch + wait complete it."""
+    import ctypes as C
+
+    from paper_2507_11916_b200 import _native
+
+    W = np.random.default_rng(6).uniform(-0.1, 0.1, (1, 21, 480)).astype(np.float32)
+    packed = bida.random_walks("rc", 777, 0, 30, seed=8)
+    L = _native.lib()
+    with bida.LinearModelBackend("rc", W, 21, 0.5) as be:
+        b, buf = C.c_void_p(), C.c_void_p()
+        _native.check(L.bida_gpu_batch_begin(be._h, len(packed), C.byref(b), C.byref(buf)))
+        C.memmove(buf, packed.ctypes.data, packed.nbytes)
+        _native.check(L.bida_gpu_batch_launch(b))
+        h = np.empty(len(packed), np.int32)
+        _native.check(L.bida_gpu_batch_wait(b, h.ctypes.data_as(C.c_void_p)))
+    assert (h == Oracle().linear_evaluate(RC, W, 0.5, packed)).all()
