@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <iterator>
@@ -137,7 +138,16 @@ struct bida_gpu_evaluator {
 
 namespace {
 
-constexpr int64_t kMaxSlot = int64_t(1) << 18;
+constexpr int64_t kMaxSlotDefault = int64_t(1) << 18;
+// BIDA_GPU_CHUNK_LOG2 (experiments): pipelined chunk size 2^k states, 12..22
+int64_t max_slot() {
+    static const int64_t v = [] {
+        const char *s = std::getenv("BIDA_GPU_CHUNK_LOG2");
+        const int k = s ? std::atoi(s) : 0;
+        return k >= 12 && k <= 22 ? int64_t(1) << k : kMaxSlotDefault;
+    }();
+    return v;
+}
 // Batches up to this size skip the copy engines: the kernel reads the packed
 // states from mapped pinned memory and writes h straight back into it (one
 // launch + one stream sync per call; search batches are 1-8K states).
@@ -326,7 +336,7 @@ int collect_errors(bida_gpu_evaluator *ev, int ch) {
 }
 
 int ensure_slots(bida_gpu_evaluator *ev, int64_t n) {
-    const int64_t want = std::min<int64_t>(std::max<int64_t>(n, 1024), kMaxSlot);
+    const int64_t want = std::min<int64_t>(std::max<int64_t>(n, 1024), max_slot());
     if (ev->slot_cap >= want)
         return BIDA_OK;
     int64_t cap = 1024;
