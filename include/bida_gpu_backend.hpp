@@ -201,7 +201,7 @@ public:
 
     bool needs_features() const override { return false; }
 #ifdef BIDA_RING_EVALUATOR
-    int max_concurrent_calls() const override { return 4; }
+    int max_concurrent_calls() const override { return 8; }  // one per zero-copy lane
     // Asynchronous path (ring agents keep several batches in flight each):
     // the packed batch is copied into a zero-copy lane at submit; the GPU writes
     // h into mapped host memory; complete() waits, copies and releases the lane.
