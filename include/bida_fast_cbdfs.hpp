@@ -43,6 +43,8 @@
 #include <thread>
 #include <vector>
 
+#include "bida_fast_apply.hpp"
+
 namespace bida {
 
 namespace fast_cbdfs {
@@ -164,7 +166,7 @@ public:
             for (int i = 0; i < n; ++i) {
                 const typename D::Action a = acts[static_cast<std::size_t>(i)];
                 FastFrame<D> fr;
-                fr.state = D::apply(parent.state, a);
+                fr.state = bida_fast::apply<D>(parent.state, a);  // = D::apply (bida_fast_apply.hpp)
                 ++stats_.generated;
                 if (fr.state == *shared_.goal) {
                     const std::int64_t cost = parent.g + 1;
