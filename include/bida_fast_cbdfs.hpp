@@ -26,6 +26,8 @@
 //   * ticket slots come from a per-thread pool (stable addresses, recycled
 //     once read) and are handed to the evaluator through the ring's
 //     submit_state_slot extension, which resolves them in place;
+//   * the cube's per-child move is a few byte shuffles (bida_fast_apply.hpp,
+//     identical to RubiksCube::apply);
 //   * expansions are added to the shared counter once per round-robin cycle
 //     (where the reference reads it for the budget check) instead of once per
 //     node.
