@@ -26,8 +26,6 @@
 //   * ticket slots come from a per-thread pool (stable addresses, recycled
 //     once read) and are handed to the evaluator through the ring's
 //     submit_state_slot extension, which resolves them in place;
-//   * the cube's per-child move is a few byte shuffles (bida_fast_apply.hpp,
-//     identical to RubiksCube::apply);
 //   * expansions are added to the shared counter once per round-robin cycle
 //     (where the reference reads it for the budget check) instead of once per
 //     node.
@@ -44,8 +42,6 @@
 #include <memory>
 #include <thread>
 #include <vector>
-
-#include "bida_fast_apply.hpp"
 
 namespace bida {
 
@@ -168,7 +164,7 @@ public:
             for (int i = 0; i < n; ++i) {
                 const typename D::Action a = acts[static_cast<std::size_t>(i)];
                 FastFrame<D> fr;
-                fr.state = bida_fast::apply<D>(parent.state, a);  // = D::apply (bida_fast_apply.hpp)
+                fr.state = D::apply(parent.state, a);
                 ++stats_.generated;
                 if (fr.state == *shared_.goal) {
                     const std::int64_t cost = parent.g + 1;

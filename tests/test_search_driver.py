@@ -201,12 +201,3 @@ def test_fast_pack_matches_reference_pack():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
 
-
-def test_fast_apply_matches_reference_apply():
-    """The overlay's shuffle-based cube move (include/bida_fast_apply.hpp) equals
-    RubiksCube::apply for all 18 moves on 400 K random states."""
-    exe = os.path.join(ROOT, "tests", "cpp", "bin", "apply_check")
-    if not os.path.exists(exe):
-        pytest.skip(f"{exe} not built")
-    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
-    assert out.returncode == 0, out.stdout + out.stderr
