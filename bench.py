@@ -567,6 +567,7 @@ def batch_sweep(wl, local, sizes=None):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     sizes = sizes or [1 << k for k in range(10, 21)]
+    peak = roofline_for(DEFAULT_WORKLOAD, wl, 1, 1.0).get("peak") if wl["kind"] == "mlp" else None
     be = make_backend(wl, local)
     _, fl = algorithmic(wl)
     stream = torch.cuda.current_stream()
@@ -596,9 +597,10 @@ def batch_sweep(wl, local, sizes=None):
         for _ in range(Re):
             be.evaluate(hp, out=ho)
         e2e_us = (time.perf_counter() - t0) * 1e6 / Re
+        tops = fl * B / dev_us / 1e6 if wl["kind"] == "mlp" else None
         out.append({"batch": B, "device_us_per_call": dev_us, "device_evals_per_s": B / dev_us * 1e6,
                     "e2e_us_per_call": e2e_us, "e2e_evals_per_s": B / e2e_us * 1e6,
-                    "device_tops": fl * B / dev_us / 1e6 if wl["kind"] == "mlp" else None})
+                    "device_tops": tops, "tensor_frac": tops / peak if tops and peak else None})
     be.close()
     return out
 
