@@ -188,6 +188,9 @@ int bida_gpu_trace_slots(void);
 int bida_gpu_exact_replays(bida_gpu_evaluator *ev, int64_t *out);
 /* Number of kernel launches issued by this handle so far (bench evidence). */
 int64_t bida_gpu_launch_count(const bida_gpu_evaluator *ev);
+/* How many of those launches were replays of a zero-copy lane's CUDA graph
+ * (small batches; BIDA_GPU_GRAPHS=0 disables the graphs). */
+int64_t bida_gpu_graph_launch_count(const bida_gpu_evaluator *ev);
 int bida_gpu_destroy(bida_gpu_evaluator *ev);
 
 #ifdef __cplusplus

@@ -72,6 +72,7 @@ EXPORTS = [
     "bida_gpu_trace_slots",
     "bida_gpu_exact_replays",
     "bida_gpu_launch_count",
+    "bida_gpu_graph_launch_count",
     "bida_gpu_destroy",
 ]
 
@@ -127,6 +128,8 @@ def lib() -> C.CDLL:
     L.bida_gpu_exact_replays.argtypes = [H, C.POINTER(i64)]
     L.bida_gpu_launch_count.argtypes = [H]
     L.bida_gpu_launch_count.restype = i64
+    L.bida_gpu_graph_launch_count.argtypes = [H]
+    L.bida_gpu_graph_launch_count.restype = i64
     L.bida_gpu_destroy.argtypes = [H]
     _lib = L
     return L

@@ -144,6 +144,10 @@ class _GpuBackendBase:
     def launch_count(self) -> int:
         return int(_native.lib().bida_gpu_launch_count(self._h))
 
+    def graph_launch_count(self) -> int:
+        """Launches that replayed a zero-copy lane's CUDA graph."""
+        return int(_native.lib().bida_gpu_graph_launch_count(self._h))
+
     def close(self) -> None:
         if self._h:
             _native.lib().bida_gpu_destroy(self._h)

@@ -126,7 +126,14 @@ struct bida_gpu_evaluator {
         int32_t *out = nullptr, *out_dev = nullptr;
         int64_t n = 0;
         bida_gpu_evaluator *owner = nullptr;
+        // one-kernel graph replayed for every launch on this lane
+        // (lane_launch); the node's parameters are rewritten per call
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t gexec = nullptr;
+        cudaGraphNode_t gnode = nullptr;
+        const void *gfunc = nullptr;
     } zc[kZcLanes];
+    std::atomic<int64_t> graph_launches{0};
     std::atomic<unsigned> zc_next{0};
     std::mutex err_mu;
     std::atomic<int64_t> zc_calls{0};
@@ -207,8 +214,8 @@ void *linear_thread_kernel_for(int domain, int cm) {
     }
 }
 
-int launch_linear_thread(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h,
-                         double *d_logits, cudaStream_t st, int *err) {
+void prepare_linear_thread(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h,
+                           double *d_logits, int *err, KernelLaunch *kl) {
     LinearThreadArgs a;
     a.packed = d_packed;
     a.n = n;
@@ -231,10 +238,18 @@ int launch_linear_thread(bida_gpu_evaluator *ev, const void *d_packed, int64_t n
     if (!ev->d_pdb)
         a.pdb.entries = nullptr;
     const int64_t want = (n + kLinThreads - 1) / kLinThreads;
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, ev->lin_grid_cap)));
-    void *args[] = {&a};
-    CUDA_TRY(cudaLaunchKernel(linear_thread_kernel_for(ev->domain, ev->lin_cm), dim3(grid), dim3(kLinThreads),
-                              args, small ? 0 : ev->lin_smem, st));
+    kl->func = linear_thread_kernel_for(ev->domain, ev->lin_cm);
+    kl->grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, ev->lin_grid_cap))));
+    kl->block = dim3(kLinThreads);
+    kl->smem = small ? 0 : ev->lin_smem;
+    kl->set_args(a);
+}
+
+int launch_linear_thread(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h,
+                         double *d_logits, cudaStream_t st, int *err) {
+    KernelLaunch kl;
+    prepare_linear_thread(ev, d_packed, n, d_h, d_logits, err, &kl);
+    CUDA_TRY(cudaLaunchKernel(kl.func, kl.grid, kl.block, kl.argv, kl.smem, st));
     ev->launches.fetch_add(1, std::memory_order_relaxed);
     return BIDA_OK;
 }
@@ -278,6 +293,82 @@ int launch(bida_gpu_evaluator *ev, const void *d_packed, int64_t n, int32_t *d_h
 }
 
 int *chan_err(bida_gpu_evaluator *ev, int ch) { return ev->err_dev + ch * kErrWords; }
+
+// BIDA_GPU_GRAPHS=0 turns the lane graphs off (A/B, debugging)
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char *s = std::getenv("BIDA_GPU_GRAPHS");
+        return !(s && s[0] == '0');
+    }();
+    return on;
+}
+
+void drop_lane_graph(bida_gpu_evaluator::ZcLane *ln) {
+    if (ln->gexec) cudaGraphExecDestroy(ln->gexec);
+    if (ln->graph) cudaGraphDestroy(ln->graph);
+    ln->gexec = nullptr;
+    ln->graph = nullptr;
+    ln->gnode = nullptr;
+    ln->gfunc = nullptr;
+}
+
+// One launch on a zero-copy lane. The lane's buffers never move, so the
+// launch is a one-node CUDA graph built at the lane's first use and replayed
+// afterwards with the node's parameters (n, grid, PDB, the argument struct)
+// rewritten in place: cudaGraphLaunch of an updated exec costs ~3.5 us less
+// per call than cudaLaunchKernel + the launch's own bookkeeping on the
+// search's small batches (profiles/r2_latency_breakdown_graph.jsonl).
+// Schedules that are not one plain launch (the wide MLP's scratch pool,
+// CTA-pair clusters, the warp-per-state linear kernel) launch directly.
+int lane_launch(bida_gpu_evaluator *ev, bida_gpu_evaluator::ZcLane *ln, int64_t n, int ch) {
+    if (n <= 0)
+        return BIDA_OK;
+    KernelLaunch kl;
+    bool graphable = false;
+    if (graphs_enabled()) {
+        if (ev->kind == BIDA_MODEL_MLP)
+            graphable = mlp_prepare(ev->mlp, ev->domain, ln->in_dev, n, ln->out_dev, chan_err(ev, ch),
+                                    ev->d_replays, ev->d_pdb ? &ev->pdb : nullptr, &kl) == 0;
+        else if (ev->lin_thread) {
+            prepare_linear_thread(ev, ln->in_dev, n, ln->out_dev, nullptr, chan_err(ev, ch), &kl);
+            graphable = true;
+        }
+    }
+    if (!graphable)
+        return launch(ev, ln->in_dev, n, ln->out_dev, nullptr, ln->st, chan_err(ev, ch));
+    cudaKernelNodeParams kp = {};
+    kp.func = const_cast<void *>(kl.func);
+    kp.gridDim = kl.grid;
+    kp.blockDim = kl.block;
+    kp.sharedMemBytes = static_cast<unsigned>(kl.smem);
+    kp.kernelParams = kl.argv;
+    kp.extra = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (ln->gexec && ln->gfunc == kl.func) {
+        e = cudaGraphExecKernelNodeSetParams(ln->gexec, ln->gnode, &kp);
+    } else {
+        drop_lane_graph(ln);
+        e = cudaGraphCreate(&ln->graph, 0);
+        if (e == cudaSuccess)
+            e = cudaGraphAddKernelNode(&ln->gnode, ln->graph, nullptr, 0, &kp);
+        if (e == cudaSuccess)
+            e = cudaGraphInstantiate(&ln->gexec, ln->graph, 0);
+        if (e == cudaSuccess)
+            ln->gfunc = kl.func;
+    }
+    if (e == cudaSuccess)
+        e = cudaGraphLaunch(ln->gexec, ln->st);
+    if (e != cudaSuccess) {
+        // a graph-path failure is not fatal: drop the graph, clear the
+        // sticky-free error and launch directly
+        drop_lane_graph(ln);
+        (void)cudaGetLastError();
+        return launch(ev, ln->in_dev, n, ln->out_dev, nullptr, ln->st, chan_err(ev, ch));
+    }
+    ev->launches.fetch_add(1, std::memory_order_relaxed);
+    ev->graph_launches.fetch_add(1, std::memory_order_relaxed);
+    return BIDA_OK;
+}
 
 // First free zero-copy lane from a rotating start; spins (then yields) while
 // every lane is busy.
@@ -410,6 +501,7 @@ void release(bida_gpu_evaluator *ev) {
     if (ev->err_host) cudaFreeHost(ev->err_host);
     for (auto &ln : ev->zc) {
         if (ln.st) cudaStreamSynchronize(ln.st);
+        drop_lane_graph(&ln);
         if (ln.done) cudaEventDestroy(ln.done);
         if (ln.in) cudaFreeHost(ln.in);
         if (ln.out) cudaFreeHost(ln.out);
@@ -740,7 +832,7 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         const int pbz = packed_bytes(ev->domain);
         std::memcpy(ln->in, packed, static_cast<size_t>(n) * pbz);
         const int ch = static_cast<int>(ln - ev->zc);
-        int rc = launch(ev, ln->in_dev, n, ln->out_dev, nullptr, ln->st, chan_err(ev, ch));
+        int rc = lane_launch(ev, ln, n, ch);
         if (rc == BIDA_OK) {
             const cudaError_t e = cudaStreamSynchronize(ln->st);
             if (e != cudaSuccess)
@@ -883,7 +975,7 @@ int bida_gpu_batch_launch(bida_gpu_batch *b) {
     if (e != cudaSuccess)
         rc = fail(BIDA_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
     if (rc == BIDA_OK)
-        rc = launch(ev, ln->in_dev, ln->n, ln->out_dev, nullptr, ln->st, chan_err(ev, ch));
+        rc = lane_launch(ev, ln, ln->n, ch);
     if (rc == BIDA_OK) {
         e = cudaEventRecord(ln->done, ln->st);
         if (e != cudaSuccess)
@@ -916,7 +1008,7 @@ int bida_gpu_submit(bida_gpu_evaluator *ev, const void *packed, int64_t n, bida_
     if (n > 0)
         std::memcpy(ln->in, packed, static_cast<size_t>(n) * packed_bytes(ev->domain));
     ln->n = n;
-    int rc = launch(ev, ln->in_dev, n, ln->out_dev, nullptr, ln->st, chan_err(ev, ch));
+    int rc = lane_launch(ev, ln, n, ch);
     if (rc == BIDA_OK) {
         const cudaError_t e = cudaEventRecord(ln->done, ln->st);
         if (e != cudaSuccess)
@@ -1151,6 +1243,10 @@ int bida_gpu_exact_replays(bida_gpu_evaluator *ev, int64_t *out) {
 
 int64_t bida_gpu_launch_count(const bida_gpu_evaluator *ev) {
     return ev ? ev->launches.load(std::memory_order_relaxed) : 0;
+}
+
+int64_t bida_gpu_graph_launch_count(const bida_gpu_evaluator *ev) {
+    return ev ? ev->graph_launches.load(std::memory_order_relaxed) : 0;
 }
 
 int bida_gpu_destroy(bida_gpu_evaluator *ev) {

@@ -1535,6 +1535,58 @@ int mlp_launch(MlpModel *m, int domain, const void *d_packed, int64_t n, int32_t
     return rc;
 }
 
+namespace {
+template <int DOMAIN, int CM>
+int prepare_t(MlpModel *m, const MlpParams &p, KernelLaunch *out) {
+    auto kern = mlp_fused_kernel<DOMAIN, CM>;
+    std::call_once(m->attr_once, [&] {
+        m->attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(m->smem));
+    });
+    if (m->attr_err != cudaSuccess)
+        return 1;
+    const long long ntiles = (p.n + kTileM - 1) / kTileM;
+    out->func = reinterpret_cast<const void *>(kern);
+    out->grid = dim3(static_cast<unsigned>(std::max<long long>(1, std::min<long long>(ntiles, m->grid_cap))));
+    out->block = dim3(kMlpThreads);
+    out->smem = m->smem;
+    out->set_args(p);
+    return 0;
+}
+template <int DOMAIN>
+int prepare_d(MlpModel *m, const MlpParams &p, KernelLaunch *out) {
+    switch (m->cm) {
+    case 32: return prepare_t<DOMAIN, 32>(m, p, out);
+    case 64: return prepare_t<DOMAIN, 64>(m, p, out);
+    default: return prepare_t<DOMAIN, 256>(m, p, out);
+    }
+}
+} // namespace
+
+int mlp_prepare(MlpModel *m, int domain, const void *d_packed, int64_t n, int32_t *d_h, int *err_dev,
+                unsigned long long *replays, const PdbArgs *pdb, KernelLaunch *out) {
+    if (m->p.mode == kWide || m->p.cluster != 1 || m->trace)
+        return 1;
+    MlpParams p = m->p;
+    if (pdb)
+        p.pdb = *pdb;
+    else
+        p.pdb.entries = nullptr;
+    p.trace = nullptr;
+    p.packed = d_packed;
+    p.n = n;
+    p.h_out = d_h;
+    p.logits_out = nullptr;
+    p.err = err_dev;
+    p.replays = replays;
+    switch (domain) {
+    case kSTP2: return prepare_d<kSTP2>(m, p, out);
+    case kSTP3: return prepare_d<kSTP3>(m, p, out);
+    case kSTP4: return prepare_d<kSTP4>(m, p, out);
+    default: return prepare_d<kRC>(m, p, out);
+    }
+}
+
 void mlp_destroy(MlpModel *m) {
     if (!m)
         return;

@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include "launch_spec.cuh"
 #include "pdb.cuh"
 
 namespace bida_gpu {
@@ -26,6 +27,11 @@ int mlp_create(const unsigned char *blob, size_t len, int F, double thr, int num
 int mlp_launch(MlpModel *m, int domain, const void *d_packed, int64_t n, int32_t *d_h,
                double *d_logits, int *err_dev, unsigned long long *replays, cudaStream_t st,
                std::atomic<int64_t> *launches, const PdbArgs *pdb = nullptr);
+// The same launch as data for graph replay; returns 0 when the model's
+// schedule is one plain kernel launch (fused schedules without clusters), 1
+// otherwise (wide schedule: scratch-pool ordering; CTA pairs).
+int mlp_prepare(MlpModel *m, int domain, const void *d_packed, int64_t n, int32_t *d_h, int *err_dev,
+                unsigned long long *replays, const PdbArgs *pdb, KernelLaunch *out);
 void mlp_destroy(MlpModel *m);
 // Debug: record a per-warp clock64 timeline of CTA 0 into dev_buf ([10 warps][mlp_trace_slots()]).
 void mlp_set_trace(MlpModel *m, long long *dev_buf);
