@@ -76,6 +76,47 @@ int main(int argc, char **argv) {
     std::printf("{\"what\": \"raw\", \"launch_sync_us\": %.2f, \"launch_poll_us\": %.2f, "
                 "\"empty_enqueue_us\": %.2f, \"empty_back_to_back_gpu_us\": %.2f}\n",
                 launch_sync, launch_poll, enqueue, ems * 1000.0 / reps);
+    {   // CUDA graph replay of the same empty kernel (north star: graph replay for small batches)
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+        empty_kernel<<<1, 32, 0, st>>>();
+        cudaStreamEndCapture(st, &g);
+        cudaGraphInstantiate(&ge, g, 0);
+        for (int i = 0; i < 100; ++i) {
+            cudaGraphLaunch(ge, st);
+            cudaStreamSynchronize(st);
+        }
+        t0 = now_us();
+        for (int i = 0; i < reps; ++i) {
+            cudaGraphLaunch(ge, st);
+            cudaStreamSynchronize(st);
+        }
+        const double graph_sync = (now_us() - t0) / reps;
+        // graph of the flag kernel + host spin
+        cudaGraph_t g2;
+        cudaGraphExec_t ge2;
+        *flag_h = 0;
+        cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+        flag_kernel<<<1, 1, 0, st>>>(flag_d, 1);
+        cudaStreamEndCapture(st, &g2);
+        cudaGraphInstantiate(&ge2, g2, 0);
+        t0 = now_us();
+        for (int i = 0; i < reps; ++i) {
+            *flag_h = 0;
+            cudaGraphLaunch(ge2, st);
+            while (*reinterpret_cast<volatile int *>(flag_h) != 1) {
+            }
+        }
+        const double graph_poll = (now_us() - t0) / reps;
+        cudaStreamSynchronize(st);
+        std::printf("{\"what\": \"graph\", \"graph_launch_sync_us\": %.2f, \"graph_launch_poll_us\": %.2f}\n",
+                    graph_sync, graph_poll);
+        cudaGraphExecDestroy(ge);
+        cudaGraphExecDestroy(ge2);
+        cudaGraphDestroy(g);
+        cudaGraphDestroy(g2);
+    }
 
     bida_gpu_evaluator *ev = nullptr;
     int rc;
@@ -143,9 +184,59 @@ int main(int argc, char **argv) {
         cudaEventSynchronize(b);
         float ms = 0;
         cudaEventElapsedTime(&ms, a, b);
+        // the same evaluation captured once into a CUDA graph and replayed
+        // (kernel parameters fixed at capture; what a per-lane graph cache costs)
+        double graph_sync = -1.0, setp_sync = -1.0;
+        {
+            cudaGraph_t g;
+            cudaGraphExec_t ge;
+            if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+                bida_gpu_evaluate_device(ev, d_in, B, d_h, nullptr, st);
+                if (cudaStreamEndCapture(st, &g) == cudaSuccess && cudaGraphInstantiate(&ge, g, 0) == cudaSuccess) {
+                    for (int i = 0; i < 20; ++i) {
+                        cudaGraphLaunch(ge, st);
+                        cudaStreamSynchronize(st);
+                    }
+                    t0 = now_us();
+                    for (int i = 0; i < r; ++i) {
+                        cudaGraphLaunch(ge, st);
+                        cudaStreamSynchronize(st);
+                    }
+                    graph_sync = (now_us() - t0) / r;
+                    // + a kernel-node parameter update before every replay
+                    size_t nn = 0;
+                    cudaGraphGetNodes(g, nullptr, &nn);
+                    std::vector<cudaGraphNode_t> nodes(nn);
+                    cudaGraphGetNodes(g, nodes.data(), &nn);
+                    cudaKernelNodeParams kp{};
+                    cudaGraphNode_t kn = nullptr;
+                    for (auto nd : nodes) {
+                        cudaGraphNodeType ty;
+                        cudaGraphNodeGetType(nd, &ty);
+                        if (ty == cudaGraphNodeTypeKernel) {
+                            kn = nd;
+                            cudaGraphKernelNodeGetParams(nd, &kp);
+                        }
+                    }
+                    if (kn) {
+                        t0 = now_us();
+                        for (int i = 0; i < r; ++i) {
+                            cudaGraphExecKernelNodeSetParams(ge, kn, &kp);
+                            cudaGraphLaunch(ge, st);
+                            cudaStreamSynchronize(st);
+                        }
+                        setp_sync = (now_us() - t0) / r;
+                    }
+                    cudaGraphExecDestroy(ge);
+                    cudaGraphDestroy(g);
+                }
+            }
+            cudaGetLastError();
+        }
         std::printf("{\"what\": \"%s\", \"batch\": %d, \"capi_us\": %.2f, \"device_launch_sync_us\": %.2f, "
-                    "\"device_back_to_back_us\": %.2f, \"device_enqueue_us\": %.2f}\n",
-                    kind, B, capi, dev_sync, ms * 1000.0 / r, enq);
+                    "\"device_back_to_back_us\": %.2f, \"device_enqueue_us\": %.2f, \"graph_replay_sync_us\": %.2f, "
+                    "\"graph_setparams_replay_sync_us\": %.2f}\n",
+                    kind, B, capi, dev_sync, ms * 1000.0 / r, enq, graph_sync, setp_sync);
     }
     bida_gpu_destroy(ev);
     return 0;
