@@ -90,6 +90,9 @@ struct MlpParams {
     int stage_bytes;    // wide: bytes per weight/activation stage
     int bias_bytes;     // wide: whole bias vector staged in shared memory (0: read from global)
     int l2hint;         // wide: evict_last L2 policy on scratch stores and stage copies
+    int bias_fold;      // resident: biases folded into each layer's accumulator by one
+                        // extra MMA K step (bias digits x a constant A block at cA_off)
+    int cA_off;         // resident + bias_fold: constant A block offset in the weight image
 };
 
 constexpr int kTraceSlots = 256;
@@ -200,20 +203,29 @@ __device__ __forceinline__ void requant_block(uint32_t t_row, int t0, const int3
 // Hidden-layer epilogue into shared memory for the fused schedules (L1-hit
 // bias): the TMEM load of the next 16 columns is in flight while the current
 // 16 are requantised and stored.  Columns [c_beg, c_end) of this thread's row.
+// BIAS = false: the accumulator already holds the bias (MlpParams::bias_fold).
+template <bool BIAS>
 __device__ __forceinline__ void requant_pipelined(uint32_t t_row, const int32_t *bias, int sh, uint32_t out, int row,
                                                   int c_beg, int c_end) {
     auto requant = [&](const int32_t(&r)[16], const int4(&b4)[4], int c0) {
         uint32_t w[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)  // saturated to u8 0..255
-            w[q] = sm100::pack_sat_u8x4((r[q * 4 + 0] + b4[q].x) >> sh, (r[q * 4 + 1] + b4[q].y) >> sh,
-                                        (r[q * 4 + 2] + b4[q].z) >> sh, (r[q * 4 + 3] + b4[q].w) >> sh);
+        for (int q = 0; q < 4; ++q) {  // saturated to u8 0..255
+            if constexpr (BIAS)
+                w[q] = sm100::pack_sat_u8x4((r[q * 4 + 0] + b4[q].x) >> sh, (r[q * 4 + 1] + b4[q].y) >> sh,
+                                            (r[q * 4 + 2] + b4[q].z) >> sh, (r[q * 4 + 3] + b4[q].w) >> sh);
+            else
+                w[q] = sm100::pack_sat_u8x4(r[q * 4 + 0] >> sh, r[q * 4 + 1] >> sh, r[q * 4 + 2] >> sh,
+                                            r[q * 4 + 3] >> sh);
+        }
         sm100::st_shared_v4(out + (c0 >> 4) * 2048u + row * 16u, w[0], w[1], w[2], w[3]);
     };
     auto load_bias = [&](int4(&b4)[4], int c0) {
+        if constexpr (BIAS) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-            b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
+            for (int q = 0; q < 4; ++q)
+                b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
+        }
     };
     int32_t ra[16], rb[16];
     int4 ba[4], bb[4];
@@ -458,6 +470,12 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                 tmem + (mode == kPair ? sl * 256u : (mode == kResident && tdbl ? (job & 1) * 256u : 0u));
                             // descriptor of k-step 0; k-step i adds i*4096 B (A) / i*cbytes (B)
                             uint64_t adesc = sm100::make_smem_desc(abase, 2048u, 128u);
+                            const bool fold = mode == kResident && p.bias_fold;
+                            if (fold && sm100::elect_one())  // D = bias (digits x constant A), then += X.W
+                                sm100::mma_i8(dcol, sm100::make_smem_desc(sW + static_cast<uint32_t>(p.cA_off), 2048u, 128u),
+                                              sm100::make_smem_desc(sW + static_cast<uint32_t>(ly.woff) + nch * cbytes,
+                                                                    cbytes >> 1, 128u),
+                                              idesc_a, 0u);
                             for (int kc = 0; kc < nch; kc += cps) {
                                 const int cnt = min(cps, nch - kc);
                                 uint32_t stg;
@@ -471,7 +489,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                 uint64_t bdesc = sm100::make_smem_desc(stg, cbytes >> 1, 128u);
                                 if (sm100::elect_one()) {
                                     for (int j = 0; j < cnt; ++j) {
-                                        const uint32_t acc = (kc + j) > 0 ? 1u : 0u;
+                                        const uint32_t acc = (fold || kc + j > 0) ? 1u : 0u;
                                         sm100::mma_i8(dcol, adesc, bdesc, idesc_a, acc);
                                         if (ly.N > 256)  // second N half: B rows 256.., D columns 256..
                                             sm100::mma_i8(dcol + 256, adesc, bdesc + (256u * 128u / 8u >> 4), idesc_b, acc);
@@ -601,7 +619,10 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                         const uint32_t out = ((l + 1) & 1) ? sY : sX;
                         const int half = mode == kPair ? ly.N : ly.N / 2;
                         const int c_beg = mode == kPair ? 0 : grp * half, c_end = c_beg + half;
-                        requant_pipelined(t_row, bias, ly.shift, out, row, c_beg, c_end);
+                        if (p.bias_fold)
+                            requant_pipelined<false>(t_row, bias, ly.shift, out, row, c_beg, c_end);
+                        else
+                            requant_pipelined<true>(t_row, bias, ly.shift, out, row, c_beg, c_end);
                         sm100::tc_fence_before();
                         sm100::fence_proxy_async_smem();
                         tr(70 + l);
@@ -615,10 +636,12 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                 if (c0 < p.C) {
                                     int32_t r[16];
                                     sm100::tmem_ld16(t_row + c0, r);
-                                    int4 b4[4];
+                                    int4 b4[4] = {};
+                                    if (!p.bias_fold) {
 #pragma unroll
-                                    for (int q = 0; q < 4; ++q)
-                                        b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
+                                        for (int q = 0; q < 4; ++q)
+                                            b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
+                                    }
                                     sm100::tmem_wait_ld();
 #pragma unroll
                                     for (int q = 0; q < 4; ++q) {
@@ -1350,6 +1373,22 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     for (uint32_t l = 0; l < L; ++l)
         Kmax = std::max(Kmax, Hp[l]);
     const bool fit_res = Nmax <= 256 && set1 + p.wbytes_pad + bar_bytes <= budget;
+    // Resident models whose biases fit |b| <= kFoldMax fold them into the
+    // accumulators: one extra K step per layer multiplies a constant A block
+    // (column 0 = 1, columns 1..31 = 255) by the bias written as s8 digits, so
+    // the epilogues skip the per-column bias loads and adds
+    // (BIDA_MLP_BIAS_FOLD=0 disables).  Integer sums: the result is identical.
+    constexpr long long kFoldMax = 127 + 255LL * 31 * 127;
+    size_t fold_bytes = kTileM * kKChunk;  // the constant A block
+    bool fold_ok = true;
+    for (int32_t v : bias)
+        fold_ok = fold_ok && std::llabs(static_cast<long long>(v)) <= kFoldMax;
+    for (uint32_t e = 0; e < E; ++e)
+        for (int l = 0; l < nl; ++l)
+            fold_bytes += static_cast<size_t>(p.layer[e][l].N) * kKChunk;
+    const int fold_pad = static_cast<int>((wtotal + fold_bytes + 1023) & ~static_cast<size_t>(1023));
+    const char *fv = std::getenv("BIDA_MLP_BIAS_FOLD");
+    fold_ok = fold_ok && !(fv && fv[0] == '0') && Nmax <= 256 && set1 + fold_pad + bar_bytes <= budget;
     const bool fit_pair = Nmax <= 256 && stages_for(2 * set1) >= 2;
     const bool want_split = fm == "split" && stages_for(set1) >= 2;
     const bool fit_split = Nmax <= 512 && stages_for(set1) >= 2;
@@ -1386,6 +1425,12 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
         p.mode = kResident;
         p.stages = 0;
         p.tmem_cols = 512u;
+        if (fold_ok) {
+            p.bias_fold = 1;
+            p.wbytes = static_cast<int>(wtotal + fold_bytes);
+            p.wbytes_pad = fold_pad;
+            p.cA_off = static_cast<int>(wtotal + fold_bytes - kTileM * kKChunk);
+        }
         m->smem = set1 + p.wbytes_pad + bar_bytes;
     } else if (!want_split && fit_pair) {
         p.mode = kPair;
@@ -1404,7 +1449,7 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     // Weight image, per layer in MMA consumption order: nh N-halves (2 for the
     // split schedule's hidden layers, else 1), each K/32 chunks of
     // [2 K-halves][N/nh/8 row groups][8 rows][16 bytes] (UMMA K-major, no swizzle).
-    img.assign(wtotal, 0);
+    img.assign(p.bias_fold ? static_cast<size_t>(p.wbytes) : wtotal, 0);
     {
         size_t pos0 = 0;
         for (int e = 0; e < static_cast<int>(E); ++e)
@@ -1460,7 +1505,29 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
                             }
                         }
                 pos0 += static_cast<size_t>(ly.N) * ly.K;
+                if (p.bias_fold) {
+                    // bias chunk after the layer's K/32 chunks: b = d0 + 255 * (d1 + ... + d31)
+                    for (int n = 0; n < ly.N; ++n) {
+                        const long long b = bias[static_cast<size_t>(ly.boff) + n];
+                        long long q = (b >= 0 ? b + 127 : b - 127) / 255;
+                        int8_t d[32];
+                        d[0] = static_cast<int8_t>(b - 255 * q);
+                        for (int k = 1; k < 32; ++k) {
+                            const long long t = std::max(-127LL, std::min(127LL, q));
+                            d[k] = static_cast<int8_t>(t);
+                            q -= t;
+                        }
+                        for (int k = 0; k < 32; ++k)
+                            img[pos0 + (k / 16) * (static_cast<size_t>(ly.N) * 16) + (n / 8) * 128 + (n % 8) * 16 + (k % 16)] =
+                                static_cast<uint8_t>(d[k]);
+                    }
+                    pos0 += static_cast<size_t>(ly.N) * kKChunk;
+                }
             }
+        if (p.bias_fold)  // constant A block, K-major core-matrix layout
+            for (int r = 0; r < kTileM; ++r)
+                for (int k = 0; k < kKChunk; ++k)
+                    img[static_cast<size_t>(p.cA_off) + (k / 16) * 2048 + r * 16 + (k % 16)] = k == 0 ? 1 : 255;
     }
     // BIDA_MLP_MULTICAST=1: streaming schedules run as CTA pairs sharing weight
     // stages by TMA multicast.  Off by default: measured slower on B200 (h512
