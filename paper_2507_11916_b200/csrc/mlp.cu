@@ -450,8 +450,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                         const int nch = ly.K / kKChunk;
                         const int cps = mode == kResident ? nch : ly.cps;
                         const uint32_t cbytes = static_cast<uint32_t>(ly.N) * kKChunk;
-                        const uint32_t idesc_a = sm100::make_idesc_i8(ly.N < 256 ? ly.N : 256);
-                        const uint32_t idesc_b = sm100::make_idesc_i8(ly.N > 256 ? ly.N - 256 : 16);
+                        // pair / resident schedules: every layer is <= 256 wide (one MMA per K step)
+                        const uint32_t idesc_a = sm100::make_idesc_i8(ly.N);
                         for (int sl = 0; sl < per && k0 + sl < nloc; ++sl) {
                             if (lane_id() == 0)
                                 tr(10 + l + 4 * sl);
@@ -491,8 +491,6 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                     for (int j = 0; j < cnt; ++j) {
                                         const uint32_t acc = (fold || kc + j > 0) ? 1u : 0u;
                                         sm100::mma_i8(dcol, adesc, bdesc, idesc_a, acc);
-                                        if (ly.N > 256)  // second N half: B rows 256.., D columns 256..
-                                            sm100::mma_i8(dcol + 256, adesc, bdesc + (256u * 128u / 8u >> 4), idesc_b, acc);
                                         adesc += 4096u >> 4;
                                         bdesc += cbytes >> 4;
                                     }

@@ -75,12 +75,13 @@ __global__ void __launch_bounds__(128, 1) bench(int n_mma, int N, int layout, lo
 // traffic slow the tensor core's operand reads?  ts=1: A from TMEM instead.
 __global__ void __launch_bounds__(512, 1) contention(int n_mma, int N, int sts_warps, int ts, long long *out) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, bar2;
     __shared__ uint32_t tslot;
     __shared__ volatile int stop;
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         sm100::mbar_init(&bar, 1);
+        sm100::mbar_init(&bar2, 1);
         sm100::fence_barrier_init();
         stop = 0;
     }
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(512, 1) contention(int n_mma, int N, int sts_w
             for (int i = 0; i < n_mma; ++i) {
                 const int ks = i & 3;
                 const uint64_t b = sm100::make_smem_desc(sB + ks * (N * 32u), N * 16u, 128u);
-                if (ts) {
+                if (ts == 1) {
                     // A operand in TMEM columns [256 + 8ks, +8): 128 lanes x 32 int8
                     asm volatile(
                         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -117,12 +118,24 @@ __global__ void __launch_bounds__(512, 1) contention(int n_mma, int N, int sts_w
             sm100::mbar_wait(&bar, 0);
             out[blockIdx.x] = clock64() - t0;
             stop = 1;
+            sm100::mbar_arrive(&bar2);
         }
     } else if (warp <= sts_warps) {
-        const uint32_t base = sm100::smem_u32(smem) + 64 * 1024 + (warp - 1) * 512 + (threadIdx.x & 31) * 16;
-        while (!stop)
-            for (int r = 0; r < 16; ++r)
-                sm100::st_shared_v4(base, r, r, r, r);
+        if (ts >= 2) {
+            // ts 2: waiting epilogue warps polling an mbarrier (mbarrier.try_wait
+            // loop, as mbar_wait does); ts 3: same with a 64 ns sleep per poll
+            while (!stop) {
+                if (sm100::mbar_try_wait(&bar2, 0))
+                    break;
+                if (ts == 3)
+                    __nanosleep(64);
+            }
+        } else {
+            const uint32_t base = sm100::smem_u32(smem) + 64 * 1024 + (warp - 1) * 512 + (threadIdx.x & 31) * 16;
+            while (!stop)
+                for (int r = 0; r < 16; ++r)
+                    sm100::st_shared_v4(base, r, r, r, r);
+        }
     }
     __syncwarp();
     sm100::tc_fence_before();
@@ -359,8 +372,8 @@ int main(int argc, char **argv) {
             }
         }
     cudaFuncSetAttribute(contention, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    for (int ts = 0; ts < 2; ++ts)
-        for (int N : {128, 256})
+    for (int ts = 0; ts < 4; ++ts)
+        for (int N : {32, 128, 256})
             for (int w : {0, 4, 8, 15}) {
                 const int n = 512;
                 contention<<<148, 512, 96 * 1024>>>(n, N, w, ts, d_out);
@@ -374,7 +387,8 @@ int main(int argc, char **argv) {
                 for (int g = 0; g < 148; ++g)
                     tot += h_out[g];
                 tot /= 148;
-                printf("contention A=%s N=%3d sts_warps=%2d  %.1f cyc/mma (floor %.0f)\n", ts ? "tmem" : "smem", N, w,
+                printf("contention %s N=%3d warps=%2d  %.1f cyc/mma (floor %.0f)\n",
+                       ts == 0 ? "A=smem sts" : ts == 1 ? "A=tmem sts" : ts == 2 ? "A=smem mbar-spin" : "A=smem mbar-sleep", N, w,
                        tot / n, 128.0 * N / 256.0);
             }
     {
