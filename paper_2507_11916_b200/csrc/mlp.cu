@@ -581,7 +581,9 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             const long long st = (blockIdx.x + k * gridDim.x) * kTileM + row;
             const bool valid = st < p.n;
             const uint64_t lo = nlo, hi = nhi;
+            tr(84);
             load_state(k + kstep, nlo, nhi);
+            tr(85);
             const bool bad = valid && state_bad(lo, hi);
             // PDB entry prefetched at tile start; consumed when h is written
             const int hpdb = (p.pdb.entries && reader && valid) ? pdb_fetch<DOMAIN>(p.pdb, lo) : 0;
@@ -590,6 +592,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             const bool live = valid && !bad;
             int hmin = 0x7fffffff;
             bool dist_bad = false;
+            tr(86);
             for (int e = 0; e < p.E; ++e, ++job) {
                 const uint32_t tcol = mode == kPair ? sl * 256u : (mode == kResident && tdbl ? (job & 1) * 256u : 0u);
                 const uint32_t t_row = tmem + tcol + (static_cast<uint32_t>(quad * 32) << 16);

@@ -35,7 +35,8 @@ torch.cuda.synchronize()
 t = buf.cpu().numpy().reshape(32, slots)
 t0 = min(int(x) >> 8 for x in t.ravel() if x and (int(x) & 0xFF) != 90)
 names = {10: "mma wait act L", 20: "mma got act L", 30: "mma commit L", 40: "epi encode", 41: "epi enc done",
-         50: "epi wait d L", 60: "epi got d L", 70: "epi hidden done L", 80: "epi readout done"}
+         50: "epi wait d L", 60: "epi got d L", 70: "epi hidden done L", 80: "epi readout done",
+         84: "tile top", 85: "next state load issued", 86: "tile setup done"}
 for w in [int(x) for x in a.warps.split(",")]:
     print(f"--- warp {w}")
     for x in t[w]:
@@ -49,4 +50,4 @@ for w in [int(x) for x in a.warps.split(",")]:
         if tag in (81, 82, 83):
             print(f"{(int(x) >> 8) - t0:9d}  readout mark {tag}")
             continue
-        print(f"{(int(x) >> 8) - t0:9d}  {names[base]}{tag - base if base not in (40, 41, 80) else ''}")
+        print(f"{(int(x) >> 8) - t0:9d}  {names[base]}{tag - base if base not in (40, 41, 80, 84, 85, 86) else ''}")
