@@ -140,6 +140,7 @@ class GpuBackend final : public bida::EvaluatorBackend<D>
 #ifdef BIDA_RING_EVALUATOR
     , public bida::ConcurrentBackend  // the C-ABI handle is re-entrant (8 zero-copy lanes)
     , public bida::AsyncEvaluatorBackend<D>  // bida_gpu_submit / bida_gpu_batch_wait
+    , public bida::GatherEvaluatorBackend<D>  // ring ranges packed in place into a lane
 #endif
 {
 public:
@@ -223,6 +224,39 @@ public:
         calls_.fetch_add(1, std::memory_order_relaxed);
         items_.fetch_add(n, std::memory_order_relaxed);
         return b;
+    }
+    // The ring agent's claimed ranges, packed in place into one zero-copy lane.
+    void evaluate_parts(std::span<const std::span<const bida::BatchItem<D>>> parts, std::size_t n,
+                        std::span<std::int32_t> out) override {
+        if (n > 0 && n <= 32768) {
+            bida_gpu_batch *b = nullptr;
+            void *in = nullptr;
+            if (bida_gpu_batch_begin(handle_, static_cast<std::int64_t>(n), &b, &in) == BIDA_OK) {
+                auto *dst = static_cast<unsigned char *>(in);
+                for (const auto &part : parts)
+                    for (const auto &it : part) {
+                        Traits::pack(it.state, dst);
+                        dst += Traits::packed_bytes;
+                    }
+                int rc = bida_gpu_batch_launch(b);
+                if (rc == BIDA_OK)
+                    rc = bida_gpu_batch_wait(b, out.data());  // zero-fills out on error
+                calls_.fetch_add(1, std::memory_order_relaxed);
+                items_.fetch_add(n, std::memory_order_relaxed);
+                if (rc) {
+                    for (auto &v : out)
+                        v = 0;
+                    note_error();
+                }
+                return;
+            }
+        }
+        std::vector<bida::BatchItem<D>> flat;  // larger than a lane: one contiguous batch
+        flat.reserve(n);
+        for (const auto &part : parts)
+            for (const auto &it : part)
+                flat.push_back(bida::BatchItem<D>{nullptr, it.state, {}});
+        evaluate(flat, out);
     }
     bool ready(void *token) override { return bida_gpu_batch_ready(static_cast<bida_gpu_batch *>(token)) != 0; }
     void complete(void *token, std::span<std::int32_t> out) override {

@@ -86,6 +86,17 @@ struct AsyncEvaluatorBackend {
     virtual int max_in_flight() const = 0;                                // over all callers
 };
 
+// Opt-in gather evaluation (bida_gpu::GpuBackend): the batch given as the
+// agent's claimed ring ranges in place (one span per contiguous run, in
+// order), so a batch spanning several shards is never moved into a scratch
+// vector first.  Writes every out[i] (n = total items).
+template <class D>
+struct GatherEvaluatorBackend {
+    virtual ~GatherEvaluatorBackend() = default;
+    virtual void evaluate_parts(std::span<const std::span<const BatchItem<D>>> parts, std::size_t n,
+                                std::span<std::int32_t> out) = 0;
+};
+
 namespace ring_detail {
 inline std::int64_t now_ns() {
     return std::chrono::duration_cast<std::chrono::nanoseconds>(
@@ -169,6 +180,7 @@ public:
             // bound by the agents' per-item host work, not by round trips in
             // flight (profiles/r2_search_async_sweep.jsonl), so the default stays
             // one synchronous call per agent.
+            gather_ = dynamic_cast<GatherEvaluatorBackend<D> *>(backend_.get());
             async_ = dynamic_cast<AsyncEvaluatorBackend<D> *>(backend_.get());
             if (async_) {
                 const int env = ring_detail::env_inflight();
@@ -381,6 +393,7 @@ private:
         bool forced_partial = false;
         bool in_place = false;
         std::vector<BatchItem<D>> scratch;  // batches spanning shards or a ring end
+        std::vector<std::span<const BatchItem<D>>> parts;  // gather backends: the ranges in place
         std::vector<std::int32_t> vals;
         void *token = nullptr;              // async backend: in flight
     };
@@ -507,6 +520,22 @@ private:
             f.n = n;
             f.forced_partial = forced_partial;
             f.token = nullptr;
+            if (gather_ && !async_) {
+                // the ranges in place, straight to the backend (no staging move)
+                f.in_place = true;
+                f.parts.clear();
+                for (const Range &r : f.ranges) {
+                    const std::size_t at = r.h & mask_, first = std::min(r.n, ring_size_ - at);
+                    f.parts.emplace_back(&shards_[r.shard].items[at], first);
+                    if (first < r.n)
+                        f.parts.emplace_back(&shards_[r.shard].items[0], r.n - first);
+                }
+                f.vals.assign(n, 0);
+                gather_->evaluate_parts(f.parts, n, f.vals);
+                finish(f);
+                spare.push_back(std::move(f));
+                continue;
+            }
             const std::span<const BatchItem<D>> items = stage(f);
             if (async_ && (f.token = async_->submit(items)) != nullptr) {
                 inflight.push_back(std::move(f));
@@ -583,6 +612,7 @@ private:
     std::atomic<bool> deadline_owner_{false};
     std::atomic<bool> quiesced_{false};  // close(): closed_ set and no submit in flight
     AsyncEvaluatorBackend<D> *async_ = nullptr;  // set: agents pipeline depth_ batches each
+    GatherEvaluatorBackend<D> *gather_ = nullptr;  // set: synchronous batches evaluated in place
     int depth_ = 1;
     std::mutex claim_m_;
     std::vector<std::thread> agents_;
