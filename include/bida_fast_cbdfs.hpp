@@ -161,6 +161,8 @@ public:
             }
             std::array<typename D::Action, D::kMaxBranching> acts{};
             const int n = D::actions(parent.state, parent.last, /*prune=*/true, acts);
+            // children are submitted together after the loop (one ring reservation)
+            std::size_t nk = 0;
             for (int i = 0; i < n; ++i) {
                 const typename D::Action a = acts[static_cast<std::size_t>(i)];
                 FastFrame<D> fr;
@@ -180,10 +182,13 @@ public:
                 }
                 fr.g = parent.g + 1;
                 fr.last = a;
-                fr.slot = submit(fr.state);
+                fr.slot = pool_.get();
+                kids_[nk] = fr.state;
+                kid_slots_[nk++] = fr.slot;
                 w.stack.push_back(fr);
                 ++live_;
             }
+            group_.submit_states_slots(tid_, kids_.data(), kid_slots_.data(), nk);
             if (live_ > stats_.peak_live_frames)
                 stats_.peak_live_frames = live_;
             return StepStatus::Progress;
@@ -228,6 +233,8 @@ private:
     SearchStats &stats_;
     const ExpandHook<D> *on_expand_;
     SlotPool pool_;
+    std::array<typename D::State, D::kMaxBranching> kids_;  // one expansion's children (submit_states_slots)
+    std::array<TicketSlot *, D::kMaxBranching> kid_slots_{};
     std::uint64_t live_ = 0;
     std::uint64_t unflushed_expanded_ = 0;
 };

@@ -229,6 +229,27 @@ public:
         enqueue(state, std::move(features), Ticket(), slot);
     }
 
+    // The children of one expansion in one reservation: one tail bump and one
+    // in-flight/close handshake for all n (the per-item locked instructions
+    // are a measurable share of a searcher's time per node).  Backends that
+    // need features, and immediate evaluators, take the one-by-one path.
+    void submit_slots(const typename D::State *states, TicketSlot *const *slots, std::size_t n) {
+        if (n == 0)
+            return;
+        if (immediate_ || backend_->needs_features()) {
+            for (std::size_t i = 0; i < n; ++i) {
+                FeatureVector x;
+                if (backend_->needs_features()) {
+                    x.resize(static_cast<std::size_t>(D::feature_length()));
+                    D::encode(states[i], x.data());
+                }
+                submit_slot(states[i], std::move(x), slots[i]);
+            }
+            return;
+        }
+        enqueue_n(states, slots, n);
+    }
+
     bool needs_features() const { return backend_->needs_features(); }
 
     // Synchronous batch of one on the caller's thread (root nodes).
@@ -320,6 +341,40 @@ private:
         std::uint64_t h;
         std::size_t n;
     };
+
+    // enqueue() for n caller-owned slots at consecutive positions of the
+    // thread's shard; items are published in order (agents claim published
+    // prefixes), the last with the seq_cst store the wake check pairs with.
+    void enqueue_n(const typename D::State *states, TicketSlot *const *raws, std::size_t n) {
+        Shard &sh = shards_[ring_detail::thread_slot() % nshards_];
+        sh.inflight.fetch_add(1, std::memory_order_seq_cst);
+        if (closed_.load(std::memory_order_seq_cst)) {
+            sh.inflight.fetch_sub(1, std::memory_order_release);
+            throw std::runtime_error("Evaluator: submission after shutdown");
+        }
+        const std::uint64_t pos0 = sh.tail.fetch_add(n, std::memory_order_acq_rel);
+        for (std::size_t i = 0; i < n; ++i) {
+            const std::uint64_t pos = pos0 + i;
+            Meta &m = sh.meta[pos & mask_];
+            unsigned spins = 0;
+            while (m.seq.load(std::memory_order_acquire) != pos)
+                ring_detail::relax(spins);
+            BatchItem<D> &it = sh.items[pos & mask_];  // ticket and features left empty by finish()
+            it.state = states[i];
+            m.raw = raws[i];
+            if (timeout_us_ > 0)
+                m.t_ns = sh.head.load(std::memory_order_relaxed) == pos ? ring_detail::now_ns() : 0;
+            if (i + 1 < n)
+                m.seq.store(pos + 1, std::memory_order_release);
+            else
+                m.seq.store(pos + 1, std::memory_order_seq_cst);
+        }
+        sh.inflight.fetch_sub(1, std::memory_order_release);
+        const std::uint64_t depth = pos0 + n - sh.head.load(std::memory_order_seq_cst);
+        // as enqueue(): wake when the shard went non-empty or a wake step was crossed
+        if (depth <= n || (depth <= ring_size_ && depth / wake_step_ != (depth - n) / wake_step_))
+            wake();
+    }
 
     void enqueue(const typename D::State &state, FeatureVector features, Ticket t, TicketSlot *raw) {
         // each searcher thread stays on one shard: the tail it bumps is
@@ -664,6 +719,12 @@ public:
             D::encode(state, x.data());
         }
         e.submit_slot(state, std::move(x), slot);
+    }
+
+    // Extension (CB-DFS overlay): one expansion's children in one reservation.
+    void submit_states_slots(int thread_id, const typename D::State *states, TicketSlot *const *slots,
+                             std::size_t n) {
+        of(thread_id).submit_slots(states, slots, n);
     }
 
     bool needs_features() const { return evs_.front()->needs_features(); }
