@@ -452,7 +452,7 @@ def config1_leg(seconds, threads):
               "--count", "1", "--threads", str(threads), "--d-init", str(d_init), "--time-limit", str(seconds)]
     out = {}
     for side, exe, extra, env in (
-            ("gpu", "tools/bin/bida_search_fast", ["--mode", "gpu", "--work-num", "64", "--batch", "8192",
+            ("gpu", "tools/bin/bida_search_fast", ["--mode", "gpu", "--work-num", "256", "--batch", "8192",
                                                    "--timeout-us", "20"],
              {"BIDA_EVAL_AGENTS": "2", "BIDA_EVAL_SHARDS": "16"}),
             ("cpu_aidastar", "tools/bin/bida_search", ["--mode", "cpu", "--immediate", "--work-num", "1"], {})):

@@ -17,8 +17,8 @@ T=$(nproc)
 EXTRACT="import json,sys; r=json.loads(sys.stdin.readline()); print(json.dumps({k:r.get(k) for k in ['instance','mode','status','cost','generated','wall_s','nodes_per_s','mean_batch','thresholds','iterations','work_num','evaluators']}))"
 for k in 8 4 1 5 7; do for d in ${DINITS:-10 12 14}; do
   BIDA_EVAL_AGENTS=2 BIDA_EVAL_SHARDS=16 timeout 300 tools/bin/bida_search_fast --domain stp4 --instances /tmp/bida_korf10.txt \
-    --model linear:/tmp/bida_man4.blin --q 0.5 --first $k --count 1 --threads $T --mode gpu --work-num 64 --batch 8192 \
-    --timeout-us 20 --d-init $d --time-limit 240 | python -c "$EXTRACT" | sed "s/^{/{\"d_init\": $d, \"side\": \"gpu\", /" >> gpurun_out/korf_dinit.jsonl
+    --model linear:/tmp/bida_man4.blin --q 0.5 --first $k --count 1 --threads $T --mode gpu --work-num ${WORK_NUM:-64} --batch 8192 \
+    --timeout-us 20 --d-init $d --time-limit 240 | python -c "$EXTRACT" | sed "s/^{/{\"d_init\": $d, \"side\": \"gpu\", \"work_num_gpu\": ${WORK_NUM:-64}, /" >> gpurun_out/korf_dinit.jsonl
   timeout 300 tools/bin/bida_search --domain stp4 --instances /tmp/bida_korf10.txt \
     --model linear:/tmp/bida_man4.blin --q 0.5 --first $k --count 1 --threads $T --mode cpu --immediate --work-num 1 \
     --d-init $d --time-limit 240 | python -c "$EXTRACT" | sed "s/^{/{\"d_init\": $d, \"side\": \"cpu_aidastar\", /" >> gpurun_out/korf_dinit.jsonl
