@@ -632,6 +632,11 @@ private:
             for (std::size_t i = 0; i < r.n; ++i, ++o) {
                 BatchItem<D> &it = f.in_place ? sh.items[(r.h + i) & mask_] : f.scratch[o];
                 Meta &mt = sh.meta[(r.h + i) & mask_];
+                // caller-owned slots live in the searchers' caches: request the
+                // line for writing a few items ahead of the resolving store
+                if (i + 8 < r.n)
+                    if (TicketSlot *ahead = sh.meta[(r.h + i + 8) & mask_].raw)
+                        __builtin_prefetch(ahead, 1, 3);
                 resolve(mt.raw ? *mt.raw : *it.ticket, f.vals[o]);
                 mt.raw = nullptr;
                 it.ticket.reset();
