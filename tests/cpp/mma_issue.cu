@@ -6,20 +6,23 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <string>
 
 #include "../../paper_2507_11916_b200/csrc/sm100.cuh"
 
 using namespace bida_gpu;
 
 template <int SHAPE, int NK>
-__global__ void __launch_bounds__(128, 1) issue(int rounds, int nk_rt, int N, long long *out) {
+__global__ void __launch_bounds__(128, 1) issue(int rounds, int nk_rt, int N, long long *out, int sts) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar;
     __shared__ uint32_t tslot;
+    __shared__ volatile int stop;
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         sm100::mbar_init(&bar, 1);
         sm100::fence_barrier_init();
+        stop = 0;
     }
     for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x)
         reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
@@ -94,8 +97,17 @@ __global__ void __launch_bounds__(128, 1) issue(int rounds, int nk_rt, int N, lo
             ph ^= 1u;
             sm100::tc_fence_after();
         }
-        if (threadIdx.x == 0)
+        if (threadIdx.x == 0) {
             out[blockIdx.x] = clock64() - t0;
+            stop = 1;
+        }
+    } else if (sts) {
+        // warps 1-3 stream st.shared.v4 into a region the MMAs do not read
+        // (an epilogue writing the next tile's one-hot while the MMAs run)
+        const uint32_t base = sm100::smem_u32(smem) + 144 * 1024 + (warp - 1) * 4096 + (threadIdx.x & 31) * 16;
+        while (!stop)
+            for (int r = 0; r < 8; ++r)
+                sm100::st_shared_v4(base + (r & 7) * 512, r, r, r, r);
     }
     __syncwarp();
     sm100::tc_fence_before();
@@ -106,12 +118,12 @@ __global__ void __launch_bounds__(128, 1) issue(int rounds, int nk_rt, int N, lo
 }
 
 template <int SHAPE, int NK>
-static void run(const char *name, int N, int nk) {
+static void run(const char *name, int N, int nk, int sts = 0) {
     long long *d_out, h_out[148];
     cudaMalloc(&d_out, sizeof(h_out));
     cudaFuncSetAttribute(issue<SHAPE, NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     const int rounds = 256;
-    issue<SHAPE, NK><<<148, 128, 160 * 1024>>>(rounds, nk, N, d_out);
+    issue<SHAPE, NK><<<148, 128, 160 * 1024>>>(rounds, nk, N, d_out, sts);
     if (cudaDeviceSynchronize() != cudaSuccess) {
         printf("error\n");
         return;
@@ -121,13 +133,19 @@ static void run(const char *name, int N, int nk) {
     for (int g = 0; g < 148; ++g)
         tot += h_out[g];
     tot /= 148.0 * rounds;
-    printf("{\"shape\": \"%s\", \"N\": %d, \"k_steps\": %d, \"cycles_per_round\": %.0f, \"cycles_per_mma\": %.1f, "
-           "\"floor\": %.0f}\n",
-           name, N, nk, tot, tot / nk, 128.0 * N / 256.0);
+    printf("{\"shape\": \"%s\", \"N\": %d, \"k_steps\": %d, \"sts_warps\": %d, \"cycles_per_round\": %.0f, "
+           "\"cycles_per_mma\": %.1f, \"floor\": %.0f}\n",
+           name, N, nk, sts ? 3 : 0, tot, tot / nk, 128.0 * N / 256.0);
     cudaFree(d_out);
 }
 
-int main() {
+int main(int argc, char **argv) {
+    if (argc > 1 && std::string(argv[1]) == "sts") {
+        for (int N : {32, 128, 256})
+            for (int sts : {0, 1})
+                run<0, 16>("elect+loop, 16 unrolled", N, 16, sts);
+        return 0;
+    }
     for (int N : {32, 128}) {
         for (int nk : {4, 16}) {
             run<0, 0>("elect+loop (kernel)", N, nk);
