@@ -146,7 +146,8 @@ struct bida_gpu_evaluator {
 namespace {
 
 constexpr int64_t kMaxSlotDefault = int64_t(1) << 18;
-// BIDA_GPU_CHUNK_LOG2 (experiments): pipelined chunk size 2^k states, 12..22
+constexpr int64_t kMinChunk = int64_t(1) << 16;
+// BIDA_GPU_CHUNK_LOG2 (experiments): largest pipelined chunk 2^k states, 12..22
 int64_t max_slot() {
     static const int64_t v = [] {
         const char *s = std::getenv("BIDA_GPU_CHUNK_LOG2");
@@ -154,6 +155,23 @@ int64_t max_slot() {
         return k >= 12 && k <= 22 ? int64_t(1) << k : kMaxSlotDefault;
     }();
     return v;
+}
+// Pipelined chunk for `remaining` states: the slot capacity (2^18 states, the
+// measured best: profiles/r2_e2e_chunks.jsonl) while at least twice that
+// remains, then halving down to kMinChunk, so the last kernel + D2H, which no
+// H2D copy overlaps, is short: e2e 2.86 -> 2.94 G evals/s (h128, 4 M states).
+// Larger caps lose (2^20: 2.65 G) although bigger copies alone move faster.
+// BIDA_GPU_CHUNK_FIXED=1: fixed chunks.
+int64_t chunk_for(int64_t remaining, int64_t cap) {
+    static const bool fixed = [] {
+        const char *s = std::getenv("BIDA_GPU_CHUNK_FIXED");
+        return s && s[0] == '1';
+    }();
+    int64_t c = cap;
+    if (!fixed)
+        while (c > kMinChunk && c * 2 > remaining)
+            c >>= 1;
+    return std::min(c, remaining);
 }
 // Batches up to this size skip the copy engines: the kernel reads the packed
 // states from mapped pinned memory and writes h straight back into it (one
@@ -885,8 +903,8 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         return BIDA_OK;
     };
     int slot = 0;
-    for (int64_t i0 = 0; i0 < n && rc == BIDA_OK; i0 += ev->slot_cap, slot = (slot + 1) % kSlots) {
-        const int64_t m = std::min<int64_t>(ev->slot_cap, n - i0);
+    for (int64_t i0 = 0, m = 0; i0 < n && rc == BIDA_OK; i0 += m, slot = (slot + 1) % kSlots) {
+        m = chunk_for(n - i0, ev->slot_cap);
         if ((rc = drain(slot)))
             break;
         const void *h2d_src = src + i0 * pb;
