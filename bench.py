@@ -717,7 +717,7 @@ def main():
         "roofline": roof,
         "e2e": {"value": total_states / r["e2e_s"], "unit": "evals/s",
                 "h2d_bytes_per_step": B * PACKED[wl["domain"]] * world, "d2h_bytes_per_step": B * 4 * world,
-                "path": "bida_gpu_evaluate (C-ABI) from/to page-locked host buffers, 4 streams, 2^18-state chunks with a halving tail (H2D, kernel, D2H per chunk)"},
+                "path": "bida_gpu_evaluate (C-ABI) from/to page-locked host buffers, mapped into the device address space: one launch reads the packed states over PCIe and writes h back (direct path)"},
         "gpu_launches": int(r["launches"]),
         "clocks": r["clocks"],
         "kernel_ms_avg": r["kern_avg_ms"],

@@ -534,6 +534,14 @@ void release(bida_gpu_evaluator *ev) {
     delete ev;
 }
 
+bool direct_enabled() {
+    static const bool on = [] {
+        const char *s = std::getenv("BIDA_GPU_DIRECT");
+        return !(s && s[0] == '0');
+    }();
+    return on;
+}
+
 bool is_pinned(const void *p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -867,6 +875,34 @@ int bida_gpu_evaluate_logits(bida_gpu_evaluator *ev, const void *packed, int64_t
         rc = collect_errors(ev, ch);
         release_lane(ln);
         return rc;
+    }
+    // Page-locked caller buffers are mapped into the device's address space
+    // (unified addressing): the kernel reads the packed states over PCIe and
+    // writes h straight back, one launch for the whole batch -- no chunked
+    // copies, no per-copy overhead, no pipeline fill or drain
+    // (BIDA_GPU_DIRECT=0: always the chunked copy pipeline).
+    if (!logits_out && direct_enabled()) {
+        void *dp = nullptr, *dh = nullptr;
+        if (is_pinned(packed) && is_pinned(h_out) &&
+            cudaHostGetDevicePointer(&dp, const_cast<void *>(packed), 0) == cudaSuccess &&
+            cudaHostGetDevicePointer(&dh, h_out, 0) == cudaSuccess &&
+            reinterpret_cast<uintptr_t>(dp) % 16 == 0 && reinterpret_cast<uintptr_t>(dh) % 4 == 0) {
+            NvtxRange nvtx_d("bida_gpu_evaluate/direct");
+            std::lock_guard<std::mutex> lk(ev->mu);
+            int rc = launch(ev, dp, n, static_cast<int32_t *>(dh), nullptr, ev->stream[0], chan_err(ev, kChanPipe));
+            if (rc == BIDA_OK) {
+                const cudaError_t e = cudaStreamSynchronize(ev->stream[0]);
+                if (e != cudaSuccess)
+                    rc = fail(BIDA_ERR_CUDA, std::string("evaluate: ") + cudaGetErrorString(e));
+            }
+            if (rc != BIDA_OK) {
+                std::fill(h_out, h_out + n, 0);
+                collect_errors(ev, kChanPipe);
+                return rc;
+            }
+            return collect_errors(ev, kChanPipe);
+        }
+        (void)cudaGetLastError();  // a pointer that is not mapped: the copy pipeline below
     }
     std::lock_guard<std::mutex> lk(ev->mu);
     if (int rc = ensure_slots(ev, n)) {

@@ -23,7 +23,13 @@ packed = bida.random_walks_fast("rc", B, 0, 30, seed=5)
 hp = torch.from_numpy(packed.view(np.uint8).copy()).pin_memory()
 host = hp.numpy().view(packed.dtype)
 out = torch.empty(B, dtype=torch.int32).pin_memory().numpy()
-with bida.MlpModelBackend("rc", make_bmlp1("rc", hidden=[128, 128], classes=21, seed=2507), 0.5) as be:
+model = os.environ.get("E2E_MODEL", "h128")
+if model == "linear":
+    be = bida.LinearModelBackend("rc", np.random.default_rng(1).uniform(-0.1, 0.1, (1, 21, 480)).astype(np.float32), 21, 0.5)
+else:
+    hid = [1610, 1610] if model == "h1610" else [128, 128]
+    be = bida.MlpModelBackend("rc", make_bmlp1("rc", hidden=hid, classes=21, seed=2507), 0.5)
+with be:
     for _ in range(3):
         be.evaluate(host, out=out)
     t0 = time.perf_counter()
@@ -49,5 +55,5 @@ for _ in range(reps):
     dev.copy_(hp, non_blocking=True)
     torch.cuda.synchronize()
 whole = hp.numel() * reps / (time.perf_counter() - t0) / 1e9
-print(json.dumps({"chunk_log2": k, "e2e_evals_per_s": e2e, "e2e_h2d_gbs": e2e * 16 / 1e9,
+print(json.dumps({"model": model, "direct": os.environ.get("BIDA_GPU_DIRECT", "1"), "chunk_log2": k, "e2e_evals_per_s": e2e, "e2e_h2d_gbs": e2e * 16 / 1e9,
                   "raw_chunked_h2d_gbs": raw, "raw_whole_h2d_gbs": whole}))
