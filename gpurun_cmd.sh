@@ -1,6 +1,6 @@
 #!/bin/bash
 cd "$(dirname "$0")"
 mkdir -p gpurun_out
-rm -f gpurun_out/korf_dinit.jsonl
-WORK_NUM=256 DINITS=14 bash tests/korf_dinit_sweep.sh > gpurun_out/korf_dinit.log 2>&1
-timeout 900 python bench.py > gpurun_out/r2_bench8.json 2> gpurun_out/r2_bench8.err
+timeout 900 python bench.py > gpurun_out/r2_bench9.json 2> gpurun_out/r2_bench9.err
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r2_gputests_full5.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke3.log 2>&1
