@@ -638,8 +638,10 @@ private:
                     if (TicketSlot *ahead = sh.meta[(r.h + i + 8) & mask_].raw)
                         __builtin_prefetch(ahead, 1, 3);
                 resolve(mt.raw ? *mt.raw : *it.ticket, f.vals[o]);
-                mt.raw = nullptr;
-                it.ticket.reset();
+                // every submit rewrites raw; caller-owned slots carry no ticket: no
+                // stores to the item or meta line beyond the seq release below
+                if (it.ticket)
+                    it.ticket.reset();
                 if (!it.features.empty())
                     FeatureVector().swap(it.features);
             }
