@@ -97,6 +97,38 @@ private:
     int lanes_;
     std::atomic<int> in_flight_{0}, peak_{0}, sync_calls_{0};
 };
+// The ring's gather path (bida_gpu::GpuBackend implements it): the claimed
+// ranges arrive in place, one span per contiguous run; several agents at once.
+class GatherSim final : public EvaluatorBackend<D>, public ConcurrentBackend, public GatherEvaluatorBackend<D> {
+public:
+    void evaluate(std::span<const BatchItem<D>> batch, std::span<std::int32_t> out) override {
+        for (std::size_t i = 0; i < batch.size(); ++i)
+            out[i] = mh_.lookup(batch[i].state);
+        plain_.fetch_add(1);
+    }
+    void evaluate_parts(std::span<const std::span<const BatchItem<D>>> parts, std::size_t n,
+                        std::span<std::int32_t> out) override {
+        std::size_t o = 0;
+        for (const auto &part : parts)
+            for (const auto &it : part)
+                out[o++] = mh_.lookup(it.state);
+        if (o != n)
+            bad_.fetch_add(1);
+        gathered_.fetch_add(1);
+        if (parts.size() > 1)
+            multi_.fetch_add(1);
+    }
+    bool needs_features() const override { return false; }
+    int max_concurrent_calls() const override { return 4; }
+    int plain() const { return plain_.load(); }
+    int gathered() const { return gathered_.load(); }
+    int multi_part() const { return multi_.load(); }
+    int bad() const { return bad_.load(); }
+
+private:
+    ManhattanHeuristic<3> mh_;
+    std::atomic<int> plain_{0}, gathered_{0}, multi_{0}, bad_{0};
+};
 #endif
 void wait_all(const std::vector<Ticket> &ts, double seconds) {
     const auto end = std::chrono::steady_clock::now() + std::chrono::duration<double>(seconds);
@@ -379,6 +411,43 @@ int main() {
         ev.close();
         const SearchStats st = ev.stats_snapshot();
         CHECK(st.batches == 10 && st.batch_items == 10 * B && st.max_batch_occupancy == B);
+    }
+    { // ring only: gather backend + caller-owned slots submitted an expansion at a
+      // time (submit_slots: one reservation for up to 18 items), 4 agents over 8
+      // shards and 6 producers; every slot resolved once to its own value
+        auto gb = std::make_unique<GatherSim>();
+        GatherSim *graw = gb.get();
+        Evaluator<D> ev(std::move(gb), 64, 20, false, 4, 8);
+        constexpr int kPer = 4000;
+        std::vector<std::vector<D::State>> states(6);
+        std::vector<std::unique_ptr<TicketSlot[]>> slots(6);
+        std::vector<std::thread> th;
+        for (int k = 0; k < 6; ++k) {
+            slots[k] = std::make_unique<TicketSlot[]>(kPer);
+            th.emplace_back([&, k] {
+                std::mt19937_64 rng(500 + k);
+                for (int i = 0; i < kPer; ++i)
+                    states[k].push_back(walk(rng, 8));
+                for (int i = 0; i < kPer;) {
+                    const int m = std::min<int>(1 + static_cast<int>(rng() % 18), kPer - i);
+                    std::vector<TicketSlot *> ps;
+                    for (int j = 0; j < m; ++j)
+                        ps.push_back(&slots[k][i + j]);
+                    ev.submit_slots(&states[k][i], ps.data(), static_cast<std::size_t>(m));
+                    i += m;
+                }
+            });
+        }
+        for (auto &t : th)
+            t.join();
+        ev.close();
+        std::size_t n = 0;
+        for (int k = 0; k < 6; ++k)
+            for (int i = 0; i < kPer; ++i, ++n)
+                CHECK(slots[k][i].value.load() == mh.lookup(states[k][i]));
+        CHECK(n == 6u * kPer && ev.resolved() == n && ev.double_resolutions() == 0);
+        CHECK(graw->gathered() > 0 && graw->plain() == 0 && graw->bad() == 0 && graw->multi_part() > 0);
+        CHECK(ev.stats_snapshot().batch_items == n);
     }
     std::printf("ring evaluator: %s\n", failures ? "FAILED" : "all checks passed");
 #else
