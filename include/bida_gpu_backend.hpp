@@ -25,6 +25,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <fstream>
 #include <iterator>
@@ -141,6 +142,7 @@ class GpuBackend final : public bida::EvaluatorBackend<D>
     , public bida::ConcurrentBackend  // the C-ABI handle is re-entrant (8 zero-copy lanes)
     , public bida::AsyncEvaluatorBackend<D>  // bida_gpu_submit / bida_gpu_batch_wait
     , public bida::GatherEvaluatorBackend<D>  // ring ranges packed in place into a lane
+    , public bida::PackedGatherBackend<D>     // submitters pre-pack; packed runs copied into a lane
 #endif
 {
 public:
@@ -194,6 +196,13 @@ public:
     }
 
     ~GpuBackend() override {
+#ifdef BIDA_RING_EVALUATOR
+        if (bida::ring_detail::profile_on() && calls_.load() > 0)
+            std::fprintf(stderr, "{\"gpu_backend_profile\": {\"calls\": %llu, \"items\": %llu, \"pack_s\": %.3f, "
+                                 "\"launch_wait_s\": %.3f}}\n",
+                         (unsigned long long)calls_.load(), (unsigned long long)items_.load(),
+                         prof_pack_ns_.load() * 1e-9, prof_gpu_ns_.load() * 1e-9);
+#endif
         if (handle_)
             bida_gpu_destroy(handle_);
     }
@@ -225,12 +234,55 @@ public:
         items_.fetch_add(n, std::memory_order_relaxed);
         return b;
     }
+    std::size_t packed_bytes() const override { return Traits::packed_bytes; }
+    void pack_state(const D::State &st, unsigned char *dst) const override { Traits::pack(st, dst); }
+    // The ring agent's claimed runs of pre-packed states, copied into one zero-copy lane.
+    void evaluate_packed(std::span<const std::span<const unsigned char>> parts, std::size_t n,
+                         std::span<std::int32_t> out) override {
+        const bool prof = bida::ring_detail::profile_on();
+        const std::int64_t t0 = prof ? bida::ring_detail::now_ns() : 0;
+        bida_gpu_batch *b = nullptr;
+        void *in = nullptr;
+        int rc = BIDA_ERR_INVALID_ARGUMENT;
+        if (n > 0 && n <= 32768 && bida_gpu_batch_begin(handle_, static_cast<std::int64_t>(n), &b, &in) == BIDA_OK) {
+            auto *dst = static_cast<unsigned char *>(in);
+            for (const auto &part : parts) {
+                std::memcpy(dst, part.data(), part.size());
+                dst += part.size();
+            }
+            const std::int64_t t1 = prof ? bida::ring_detail::now_ns() : 0;
+            rc = bida_gpu_batch_launch(b);
+            if (rc == BIDA_OK)
+                rc = bida_gpu_batch_wait(b, out.data());  // zero-fills out on error
+            if (prof) {
+                prof_pack_ns_.fetch_add(t1 - t0, std::memory_order_relaxed);
+                prof_gpu_ns_.fetch_add(bida::ring_detail::now_ns() - t1, std::memory_order_relaxed);
+            }
+        } else if (n > 0) {  // larger than a lane: one contiguous staging copy
+            thread_local std::vector<unsigned char> staging;
+            staging.clear();
+            for (const auto &part : parts)
+                staging.insert(staging.end(), part.begin(), part.end());
+            rc = bida_gpu_evaluate(handle_, staging.data(), static_cast<std::int64_t>(n), out.data());
+        } else {
+            return;
+        }
+        calls_.fetch_add(1, std::memory_order_relaxed);
+        items_.fetch_add(n, std::memory_order_relaxed);
+        if (rc) {
+            for (auto &v : out)
+                v = 0;
+            note_error();
+        }
+    }
     // The ring agent's claimed ranges, packed in place into one zero-copy lane.
     void evaluate_parts(std::span<const std::span<const bida::BatchItem<D>>> parts, std::size_t n,
                         std::span<std::int32_t> out) override {
         if (n > 0 && n <= 32768) {
             bida_gpu_batch *b = nullptr;
             void *in = nullptr;
+            const bool prof = bida::ring_detail::profile_on();
+            const std::int64_t t0 = prof ? bida::ring_detail::now_ns() : 0;
             if (bida_gpu_batch_begin(handle_, static_cast<std::int64_t>(n), &b, &in) == BIDA_OK) {
                 auto *dst = static_cast<unsigned char *>(in);
                 for (const auto &part : parts)
@@ -238,9 +290,14 @@ public:
                         Traits::pack(it.state, dst);
                         dst += Traits::packed_bytes;
                     }
+                const std::int64_t t1 = prof ? bida::ring_detail::now_ns() : 0;
                 int rc = bida_gpu_batch_launch(b);
                 if (rc == BIDA_OK)
                     rc = bida_gpu_batch_wait(b, out.data());  // zero-fills out on error
+                if (prof) {
+                    prof_pack_ns_.fetch_add(t1 - t0, std::memory_order_relaxed);
+                    prof_gpu_ns_.fetch_add(bida::ring_detail::now_ns() - t1, std::memory_order_relaxed);
+                }
                 calls_.fetch_add(1, std::memory_order_relaxed);
                 items_.fetch_add(n, std::memory_order_relaxed);
                 if (rc) {
@@ -322,6 +379,7 @@ private:
 
     bida_gpu_evaluator *handle_ = nullptr;
     std::atomic<std::uint64_t> errors_{0}, calls_{0}, items_{0};
+    std::atomic<std::int64_t> prof_pack_ns_{0}, prof_gpu_ns_{0};  // BIDA_RING_PROFILE (ring builds)
     mutable std::mutex err_m_;
     std::string last_error_;
 };

@@ -42,6 +42,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <chrono>
 #include <climits>
 #include <cstdint>
@@ -97,11 +98,38 @@ struct GatherEvaluatorBackend {
                                 std::span<std::int32_t> out) = 0;
 };
 
+// Opt-in pre-packing (bida_gpu::GpuBackend): submitters pack each state into
+// the ring slot's packed bytes while the state is hot in their cache, and the
+// agent hands the backend the claimed runs of packed bytes (one span per
+// contiguous run).  With the gather path alone the agent packs, reading every
+// state from a line another core just wrote (BIDA_RING_PROFILE measured
+// ~11 ns per state there).  Writes every out[i].
+template <class D>
+struct PackedGatherBackend {
+    virtual ~PackedGatherBackend() = default;
+    virtual std::size_t packed_bytes() const = 0;
+    virtual void pack_state(const typename D::State &state, unsigned char *dst) const = 0;
+    virtual void evaluate_packed(std::span<const std::span<const unsigned char>> parts, std::size_t n,
+                                 std::span<std::int32_t> out) = 0;
+};
+
 namespace ring_detail {
 inline std::int64_t now_ns() {
     return std::chrono::duration_cast<std::chrono::nanoseconds>(
                std::chrono::steady_clock::now().time_since_epoch())
         .count();
+}
+// BIDA_RING_PROFILE=1: agents time their phases; totals go to stderr at close()
+inline bool profile_on() {
+    static const bool on = [] {
+        const char *s = std::getenv("BIDA_RING_PROFILE");
+        return s && s[0] == '1';
+    }();
+    return on;
+}
+inline bool env_noprepack() {  // BIDA_EVAL_PREPACK=0: the agent packs (gather path)
+    const char *s = std::getenv("BIDA_EVAL_PREPACK");
+    return s && s[0] == '0';
 }
 inline int default_agents() {
     const char *s = std::getenv("BIDA_EVAL_AGENTS");
@@ -181,6 +209,7 @@ public:
             // flight (profiles/r2_search_async_sweep.jsonl), so the default stays
             // one synchronous call per agent.
             gather_ = dynamic_cast<GatherEvaluatorBackend<D> *>(backend_.get());
+            packer_ = dynamic_cast<PackedGatherBackend<D> *>(backend_.get());
             async_ = dynamic_cast<AsyncEvaluatorBackend<D> *>(backend_.get());
             if (async_) {
                 const int env = ring_detail::env_inflight();
@@ -189,6 +218,13 @@ public:
                     async_ = nullptr;
                     depth_ = 1;
                 }
+            }
+            if (packer_ && (async_ || !gather_ || backend_->needs_features() || ring_detail::env_noprepack()))
+                packer_ = nullptr;
+            if (packer_) {
+                pb_ = packer_->packed_bytes();
+                for (std::size_t k = 0; k < nshards_; ++k)
+                    shards_[k].packed = std::make_unique<unsigned char[]>(ring_size_ * pb_);
             }
             for (int k = 0; k < k_agents; ++k)
                 agents_.emplace_back([this] { agent_loop(); });
@@ -293,6 +329,18 @@ public:
     void close() {
         if (closed_.exchange(true, std::memory_order_seq_cst))
             return;
+        struct Report {  // after the agents joined (end of close)
+            Evaluator *ev;
+            ~Report() {
+                if (ring_detail::profile_on() && ev->prof_batches_.load() > 0)
+                    std::fprintf(stderr,
+                                 "{\"ring_profile\": {\"agents\": %zu, \"batches\": %llu, \"items\": %llu, "
+                                 "\"claim_s\": %.3f, \"evaluate_s\": %.3f, \"finish_s\": %.3f}}\n",
+                                 ev->agents_.size(), (unsigned long long)ev->prof_batches_.load(),
+                                 (unsigned long long)ev->prof_items_.load(), ev->prof_claim_ns_.load() * 1e-9,
+                                 ev->prof_eval_ns_.load() * 1e-9, ev->prof_finish_ns_.load() * 1e-9);
+            }
+        } report{this};
         for (std::size_t k = 0; k < nshards_; ++k) {
             unsigned spins = 0;
             while (shards_[k].inflight.load(std::memory_order_seq_cst) != 0)
@@ -335,6 +383,7 @@ private:
         alignas(64) std::atomic<std::uint64_t> head{0}; // next position agents claim
         std::unique_ptr<BatchItem<D>[]> items;
         std::unique_ptr<Meta[]> meta;
+        std::unique_ptr<unsigned char[]> packed;  // pre-packing backends: pb_ bytes per slot
     };
     struct Range {
         std::size_t shard;
@@ -359,8 +408,12 @@ private:
             unsigned spins = 0;
             while (m.seq.load(std::memory_order_acquire) != pos)
                 ring_detail::relax(spins);
-            BatchItem<D> &it = sh.items[pos & mask_];  // ticket and features left empty by finish()
-            it.state = states[i];
+            if (packer_) {
+                packer_->pack_state(states[i], &sh.packed[(pos & mask_) * pb_]);
+            } else {
+                BatchItem<D> &it = sh.items[pos & mask_];  // ticket and features left empty by finish()
+                it.state = states[i];
+            }
             m.raw = raws[i];
             if (timeout_us_ > 0)
                 m.t_ns = sh.head.load(std::memory_order_relaxed) == pos ? ring_detail::now_ns() : 0;
@@ -395,6 +448,8 @@ private:
         BatchItem<D> &it = sh.items[pos & mask_];
         it.ticket = std::move(t);
         it.state = state;
+        if (packer_)
+            packer_->pack_state(state, &sh.packed[(pos & mask_) * pb_]);
         it.features = std::move(features);
         m.raw = raw;
         // only the oldest pending item's age matters (the flush deadline): an
@@ -449,6 +504,7 @@ private:
         bool in_place = false;
         std::vector<BatchItem<D>> scratch;  // batches spanning shards or a ring end
         std::vector<std::span<const BatchItem<D>>> parts;  // gather backends: the ranges in place
+        std::vector<std::span<const unsigned char>> bytes;  // pre-packing backends: packed runs
         std::vector<std::int32_t> vals;
         void *token = nullptr;              // async backend: in flight
     };
@@ -458,6 +514,7 @@ private:
         std::vector<Flight> spare;
         std::vector<Range> ranges;
         std::size_t rot = 0;
+        std::int64_t tp0 = ring_detail::profile_on() ? ring_detail::now_ns() : 0;
         auto finish_front = [&] {
             finish(inflight.front());
             spare.push_back(std::move(inflight.front()));
@@ -575,6 +632,35 @@ private:
             f.n = n;
             f.forced_partial = forced_partial;
             f.token = nullptr;
+            const std::int64_t tp1 = ring_detail::profile_on() ? ring_detail::now_ns() : 0;
+            if (tp1)
+                prof_claim_ns_.fetch_add(tp1 - tp0, std::memory_order_relaxed);
+            if (packer_) {
+                // the submitters' packed bytes, run by run, straight to the backend
+                f.in_place = true;
+                f.bytes.clear();
+                for (const Range &r : f.ranges) {
+                    const std::size_t at = r.h & mask_, first = std::min(r.n, ring_size_ - at);
+                    const unsigned char *base = shards_[r.shard].packed.get();
+                    f.bytes.emplace_back(base + at * pb_, first * pb_);
+                    if (first < r.n)
+                        f.bytes.emplace_back(base, (r.n - first) * pb_);
+                }
+                f.vals.assign(n, 0);
+                packer_->evaluate_packed(f.bytes, n, f.vals);
+                const std::int64_t tp2 = tp1 ? ring_detail::now_ns() : 0;
+                finish(f);
+                if (tp1) {
+                    const std::int64_t tp3 = ring_detail::now_ns();
+                    prof_eval_ns_.fetch_add(tp2 - tp1, std::memory_order_relaxed);
+                    prof_finish_ns_.fetch_add(tp3 - tp2, std::memory_order_relaxed);
+                    prof_batches_.fetch_add(1, std::memory_order_relaxed);
+                    prof_items_.fetch_add(n, std::memory_order_relaxed);
+                    tp0 = tp3;
+                }
+                spare.push_back(std::move(f));
+                continue;
+            }
             if (gather_ && !async_) {
                 // the ranges in place, straight to the backend (no staging move)
                 f.in_place = true;
@@ -587,7 +673,16 @@ private:
                 }
                 f.vals.assign(n, 0);
                 gather_->evaluate_parts(f.parts, n, f.vals);
+                const std::int64_t tp2 = tp1 ? ring_detail::now_ns() : 0;
                 finish(f);
+                if (tp1) {
+                    const std::int64_t tp3 = ring_detail::now_ns();
+                    prof_eval_ns_.fetch_add(tp2 - tp1, std::memory_order_relaxed);
+                    prof_finish_ns_.fetch_add(tp3 - tp2, std::memory_order_relaxed);
+                    prof_batches_.fetch_add(1, std::memory_order_relaxed);
+                    prof_items_.fetch_add(n, std::memory_order_relaxed);
+                    tp0 = tp3;
+                }
                 spare.push_back(std::move(f));
                 continue;
             }
@@ -675,6 +770,10 @@ private:
     std::atomic<bool> quiesced_{false};  // close(): closed_ set and no submit in flight
     AsyncEvaluatorBackend<D> *async_ = nullptr;  // set: agents pipeline depth_ batches each
     GatherEvaluatorBackend<D> *gather_ = nullptr;  // set: synchronous batches evaluated in place
+    PackedGatherBackend<D> *packer_ = nullptr;     // set: submitters pack, agents pass packed runs
+    std::size_t pb_ = 0;
+    std::atomic<std::int64_t> prof_claim_ns_{0}, prof_eval_ns_{0}, prof_finish_ns_{0};  // BIDA_RING_PROFILE
+    std::atomic<std::uint64_t> prof_batches_{0}, prof_items_{0};
     int depth_ = 1;
     std::mutex claim_m_;
     std::vector<std::thread> agents_;

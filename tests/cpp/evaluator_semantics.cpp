@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <array>
 #include <atomic>
+#include <cstring>
 #include <chrono>
 #include <cstdlib>
 #include <cstdio>
@@ -128,6 +129,50 @@ public:
 private:
     ManhattanHeuristic<3> mh_;
     std::atomic<int> plain_{0}, gathered_{0}, multi_{0}, bad_{0};
+};
+// The ring's pre-packing path: submitters "pack" a state into 4 bytes (here
+// its Manhattan value itself), the agent hands the claimed runs back as bytes.
+class PackedSim final : public EvaluatorBackend<D>, public ConcurrentBackend, public GatherEvaluatorBackend<D>,
+                        public PackedGatherBackend<D> {
+public:
+    void evaluate(std::span<const BatchItem<D>> batch, std::span<std::int32_t> out) override {
+        for (std::size_t i = 0; i < batch.size(); ++i)
+            out[i] = mh_.lookup(batch[i].state);
+        plain_.fetch_add(1);
+    }
+    void evaluate_parts(std::span<const std::span<const BatchItem<D>>>, std::size_t, std::span<std::int32_t> out) override {
+        for (auto &v : out)
+            v = 0;
+        gathered_.fetch_add(1);  // must not be used: the packed path wins
+    }
+    std::size_t packed_bytes() const override { return 4; }
+    void pack_state(const D::State &st, unsigned char *dst) const override {
+        const std::int32_t v = mh_.lookup(st);
+        std::memcpy(dst, &v, 4);
+    }
+    void evaluate_packed(std::span<const std::span<const unsigned char>> parts, std::size_t n,
+                         std::span<std::int32_t> out) override {
+        std::size_t o = 0;
+        for (const auto &part : parts)
+            for (std::size_t b = 0; b + 4 <= part.size(); b += 4)
+                std::memcpy(&out[o++], part.data() + b, 4);
+        if (o != n)
+            bad_.fetch_add(1);
+        packed_calls_.fetch_add(1);
+        if (parts.size() > 1)
+            multi_.fetch_add(1);
+    }
+    bool needs_features() const override { return false; }
+    int max_concurrent_calls() const override { return 4; }
+    int plain() const { return plain_.load(); }
+    int gathered() const { return gathered_.load(); }
+    int packed_calls() const { return packed_calls_.load(); }
+    int multi_part() const { return multi_.load(); }
+    int bad() const { return bad_.load(); }
+
+private:
+    ManhattanHeuristic<3> mh_;
+    std::atomic<int> plain_{0}, gathered_{0}, packed_calls_{0}, multi_{0}, bad_{0};
 };
 #endif
 void wait_all(const std::vector<Ticket> &ts, double seconds) {
@@ -448,6 +493,52 @@ int main() {
         CHECK(n == 6u * kPer && ev.resolved() == n && ev.double_resolutions() == 0);
         CHECK(graw->gathered() > 0 && graw->plain() == 0 && graw->bad() == 0 && graw->multi_part() > 0);
         CHECK(ev.stats_snapshot().batch_items == n);
+    }
+    { // ring only: pre-packing backend; reservations and single submits (tickets)
+      // mixed, 4 agents, 8 shards, 6 producers: every value lands in its own slot
+        auto pb = std::make_unique<PackedSim>();
+        PackedSim *praw = pb.get();
+        Evaluator<D> ev(std::move(pb), 64, 20, false, 4, 8);
+        constexpr int kPer = 4000;
+        std::vector<std::vector<D::State>> states(6);
+        std::vector<std::unique_ptr<TicketSlot[]>> slots(6);
+        std::vector<std::vector<std::pair<D::State, Ticket>>> tickets(6);
+        std::vector<std::thread> th;
+        for (int k = 0; k < 6; ++k) {
+            slots[k] = std::make_unique<TicketSlot[]>(kPer);
+            th.emplace_back([&, k] {
+                std::mt19937_64 rng(700 + k);
+                for (int i = 0; i < kPer; ++i)
+                    states[k].push_back(walk(rng, 8));
+                for (int i = 0; i < kPer;) {
+                    const int m = std::min<int>(1 + static_cast<int>(rng() % 18), kPer - i);
+                    std::vector<TicketSlot *> ps;
+                    for (int j = 0; j < m; ++j)
+                        ps.push_back(&slots[k][i + j]);
+                    ev.submit_slots(&states[k][i], ps.data(), static_cast<std::size_t>(m));
+                    i += m;
+                    if (rng() % 4 == 0) {
+                        const D::State s = walk(rng, 8);
+                        tickets[k].emplace_back(s, ev.submit(s, {}));
+                    }
+                }
+            });
+        }
+        for (auto &t : th)
+            t.join();
+        ev.close();
+        std::size_t n = 0;
+        for (int k = 0; k < 6; ++k) {
+            for (int i = 0; i < kPer; ++i, ++n)
+                CHECK(slots[k][i].value.load() == mh.lookup(states[k][i]));
+            for (auto &[s, t] : tickets[k]) {
+                CHECK(poll(t) == mh.lookup(s));
+                ++n;
+            }
+        }
+        CHECK(ev.resolved() == n && ev.double_resolutions() == 0);
+        CHECK(praw->packed_calls() > 0 && praw->gathered() == 0 && praw->plain() == 0 && praw->bad() == 0 &&
+              praw->multi_part() > 0);
     }
     std::printf("ring evaluator: %s\n", failures ? "FAILED" : "all checks passed");
 #else
