@@ -1,14 +1,6 @@
 #!/bin/bash
 cd "$(dirname "$0")"
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests/test_gpu_search.py tests/test_gpu_search_configs.py -q -x > gpurun_out/search_tests.log 2>&1
-rm -f gpurun_out/search_balance.jsonl
-python -c "from paper_2507_11916_b200.models import make_bmlp1; open('/tmp/h128.bmlp','wb').write(make_bmlp1('rc', hidden=[128, 128], classes=21, ensemble=1, seed=2507))"
-for rep in 1 2; do
-for c in 12_4 13_3 11_5 14_2 10_6; do
-  t=${c%_*}; a=${c#*_}
-  BIDA_EVAL_AGENTS=$a BIDA_EVAL_SHARDS=16 timeout 200 tools/bin/bida_search_fast --domain rc --walks 1:14:14:2508 \
-    --model mlp:/tmp/h128.bmlp --q 0.5 --table1-pdb 8 --pdb-build gpu --threads $t --mode gpu --gpu-pdb \
-    --work-num 128 --batch 16384 --timeout-us 25 --time-limit 120 | python -c "import json,sys; r=json.loads(sys.stdin.readline()); print(json.dumps({'threads':$t,'agents':$a, **{k:r[k] for k in ['status','generated','wall_s','nodes_per_s','mean_batch']}}))" >> gpurun_out/search_balance.jsonl
-done
-done
+timeout 900 python bench.py > gpurun_out/r2_bench10.json 2> gpurun_out/r2_bench10.err
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r2_gputests_full6.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke4.log 2>&1
