@@ -23,22 +23,24 @@
 //     the DFS has already been popped, so path_[0..d-1) is still its
 //     ancestors' actions and only path_[d-1] = frame.last changes.  The full
 //     path is materialised only when a goal is found;
-//   * ticket slots come from a per-thread pool (stable addresses, recycled
-//     once read) and are handed to the evaluator through the ring's
-//     submit_state_slot extension, which resolves them in place;
+//   * ticket slots live in a per-work arena indexed by stack position (stable
+//     addresses; an expansion's children get adjacent slots, reused once read)
+//     and are handed to the evaluator in one reservation per expansion
+//     (submit_states_slots), which resolves them in place;
 //   * expansions are added to the shared counter once per round-robin cycle
 //     (where the reference reads it for the budget check) instead of once per
 //     node.
 //
 // On stop (goal, budget, deadline) frames may still be pending in the
 // evaluator: the thread forces flushes and waits for its own slots to resolve
-// before it returns, so no evaluator thread ever writes into a released pool.
+// before it returns, so no evaluator thread ever writes into a released arena.
 #pragma once
 
 #include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstdlib>
+#include <deque>
 #include <memory>
 #include <thread>
 #include <vector>
@@ -55,29 +57,6 @@ inline int idle_sleep_us() {
     return us;
 }
 
-// Per-thread pool of write-once ticket slots with stable addresses.
-class SlotPool {
-public:
-    TicketSlot *get() {
-        if (free_.empty()) {
-            chunks_.push_back(std::make_unique<TicketSlot[]>(kChunk));
-            TicketSlot *c = chunks_.back().get();
-            for (std::size_t i = kChunk; i-- > 0;)
-                free_.push_back(c + i);
-        }
-        TicketSlot *s = free_.back();
-        free_.pop_back();
-        s->value.store(-1, std::memory_order_relaxed);
-        return s;
-    }
-    void put(TicketSlot *s) { free_.push_back(s); }
-
-private:
-    static constexpr std::size_t kChunk = 4096;
-    std::vector<std::unique_ptr<TicketSlot[]>> chunks_;
-    std::vector<TicketSlot *> free_;
-};
-
 template <class D>
 struct FastFrame {
     typename D::State state;
@@ -91,6 +70,19 @@ template <class D>
 struct FastWork {
     const WorkSeed<D> *seed = nullptr;
     std::vector<FastFrame<D>> stack;
+    // slot of the frame at stack position i: an expansion's children sit at
+    // consecutive positions, so their slots share cache lines -- the agent
+    // resolves them with one or two line transfers, and the searcher's poll of
+    // the first brings its siblings' values along.  A position is reused only
+    // after its frame was popped, i.e. after its value was read.
+    std::deque<TicketSlot> slot_arena;
+    TicketSlot *slot_at(std::size_t i) {
+        while (slot_arena.size() <= i)
+            slot_arena.emplace_back();
+        TicketSlot *t = &slot_arena[i];
+        t->value.store(-1, std::memory_order_relaxed);
+        return t;
+    }
     std::vector<typename D::Action> path;  // path[i]: action at depth i+1 below the work root
     int root_g = 0;
     bool done() const { return stack.empty(); }
@@ -114,8 +106,10 @@ public:
         f.g = static_cast<int>(seed->init_history.size());
         w.root_g = f.g;
         f.h = seed->root_h;
-        if (f.h < 0)
-            f.slot = submit(f.state);
+        if (f.h < 0) {
+            f.slot = w.slot_at(0);
+            group_.submit_state_slot(tid_, f.state, f.slot);
+        }
         f.last = seed->init_history.empty() ? D::kNoAction : seed->init_history.back();
         w.stack.push_back(f);
         ++live_;
@@ -134,7 +128,6 @@ public:
                 if (v < 0)
                     return StepStatus::Blocked;
                 top.h = v;
-                pool_.put(top.slot);
                 top.slot = nullptr;
             }
             const std::int64_t f = top.g + top.h;
@@ -182,7 +175,7 @@ public:
                 }
                 fr.g = parent.g + 1;
                 fr.last = a;
-                fr.slot = pool_.get();
+                fr.slot = w.slot_at(w.stack.size());
                 kids_[nk] = fr.state;
                 kid_slots_[nk++] = fr.slot;
                 w.stack.push_back(fr);
@@ -203,7 +196,7 @@ public:
     }
 
     // Frames still waiting on the evaluator when the round stops: wait for
-    // their slots (the pool must outlive every write into it).
+    // their slots (the arenas must outlive every write into them).
     void drain(std::vector<FastWork<D>> &slots) {
         for (;;) {
             bool pending = false;
@@ -219,11 +212,6 @@ public:
     }
 
 private:
-    TicketSlot *submit(const typename D::State &s) {
-        TicketSlot *slot = pool_.get();
-        group_.submit_state_slot(tid_, s, slot);
-        return slot;
-    }
 
     int tid_;
     std::int64_t bound_;
@@ -232,7 +220,6 @@ private:
     IterationShared<D> &shared_;
     SearchStats &stats_;
     const ExpandHook<D> *on_expand_;
-    SlotPool pool_;
     std::array<typename D::State, D::kMaxBranching> kids_;  // one expansion's children (submit_states_slots)
     std::array<TicketSlot *, D::kMaxBranching> kid_slots_{};
     std::uint64_t live_ = 0;
