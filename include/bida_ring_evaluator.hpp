@@ -199,6 +199,7 @@ public:
         // a producer wakes the agents when its shard goes nonempty or crosses
         // a multiple of capacity / shards (the agents then check the total)
         wake_step_ = std::max<std::uint64_t>(1, capacity_ / nshards_);
+        feats_ = backend_->needs_features();
         if (!immediate_) {
             const int k_agents = ring_detail::agents_for(backend_.get(), agents);
             // in-flight batches per agent: the backend's lanes shared by the
@@ -725,13 +726,18 @@ private:
         for (const Range &r : f.ranges) {
             Shard &sh = shards_[r.shard];
             for (std::size_t i = 0; i < r.n; ++i, ++o) {
-                BatchItem<D> &it = f.in_place ? sh.items[(r.h + i) & mask_] : f.scratch[o];
                 Meta &mt = sh.meta[(r.h + i) & mask_];
                 // caller-owned slots live in the searchers' caches: request the
                 // line for writing a few items ahead of the resolving store
                 if (i + 8 < r.n)
                     if (TicketSlot *ahead = sh.meta[(r.h + i + 8) & mask_].raw)
                         __builtin_prefetch(ahead, 1, 3);
+                if (mt.raw && !feats_) {
+                    // no ticket, no features: the item's line is not touched at all
+                    resolve(*mt.raw, f.vals[o]);
+                    continue;
+                }
+                BatchItem<D> &it = f.in_place ? sh.items[(r.h + i) & mask_] : f.scratch[o];
                 resolve(mt.raw ? *mt.raw : *it.ticket, f.vals[o]);
                 // every submit rewrites raw; caller-owned slots carry no ticket: no
                 // stores to the item or meta line beyond the seq release below
@@ -772,6 +778,7 @@ private:
     GatherEvaluatorBackend<D> *gather_ = nullptr;  // set: synchronous batches evaluated in place
     PackedGatherBackend<D> *packer_ = nullptr;     // set: submitters pack, agents pass packed runs
     std::size_t pb_ = 0;
+    bool feats_ = true;  // backend_->needs_features(), read once
     std::atomic<std::int64_t> prof_claim_ns_{0}, prof_eval_ns_{0}, prof_finish_ns_{0};  // BIDA_RING_PROFILE
     std::atomic<std::uint64_t> prof_batches_{0}, prof_items_{0};
     int depth_ = 1;
