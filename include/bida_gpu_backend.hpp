@@ -236,6 +236,10 @@ public:
     }
     std::size_t packed_bytes() const override { return Traits::packed_bytes; }
     void pack_state(const D::State &st, unsigned char *dst) const override { Traits::pack(st, dst); }
+    void pack_states(const D::State *st, std::size_t n, unsigned char *dst) const override {
+        for (std::size_t i = 0; i < n; ++i)
+            Traits::pack(st[i], dst + i * Traits::packed_bytes);
+    }
     // The ring agent's claimed runs of pre-packed states, copied into one zero-copy lane.
     void evaluate_packed(std::span<const std::span<const unsigned char>> parts, std::size_t n,
                          std::span<std::int32_t> out) override {

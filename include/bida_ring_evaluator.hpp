@@ -109,6 +109,11 @@ struct PackedGatherBackend {
     virtual ~PackedGatherBackend() = default;
     virtual std::size_t packed_bytes() const = 0;
     virtual void pack_state(const typename D::State &state, unsigned char *dst) const = 0;
+    // n consecutive states into n consecutive packed slots (one call per reservation run)
+    virtual void pack_states(const typename D::State *states, std::size_t n, unsigned char *dst) const {
+        for (std::size_t i = 0; i < n; ++i)
+            pack_state(states[i], dst + i * packed_bytes());
+    }
     virtual void evaluate_packed(std::span<const std::span<const unsigned char>> parts, std::size_t n,
                                  std::span<std::int32_t> out) = 0;
 };
@@ -403,6 +408,19 @@ private:
             throw std::runtime_error("Evaluator: submission after shutdown");
         }
         const std::uint64_t pos0 = sh.tail.fetch_add(n, std::memory_order_acq_rel);
+        if (packer_) {
+            // every slot of the reservation free (its previous lap consumed), then
+            // one pack call per contiguous run (two if the reservation wraps)
+            for (std::size_t i = 0; i < n; ++i) {
+                unsigned spins = 0;
+                while (sh.meta[(pos0 + i) & mask_].seq.load(std::memory_order_acquire) != pos0 + i)
+                    ring_detail::relax(spins);
+            }
+            const std::size_t at = pos0 & mask_, first = std::min(n, ring_size_ - at);
+            packer_->pack_states(states, first, &sh.packed[at * pb_]);
+            if (first < n)
+                packer_->pack_states(states + first, n - first, &sh.packed[0]);
+        }
         for (std::size_t i = 0; i < n; ++i) {
             const std::uint64_t pos = pos0 + i;
             Meta &m = sh.meta[pos & mask_];
@@ -410,7 +428,7 @@ private:
             while (m.seq.load(std::memory_order_acquire) != pos)
                 ring_detail::relax(spins);
             if (packer_) {
-                packer_->pack_state(states[i], &sh.packed[(pos & mask_) * pb_]);
+                // packed above
             } else {
                 BatchItem<D> &it = sh.items[pos & mask_];  // ticket and features left empty by finish()
                 it.state = states[i];
