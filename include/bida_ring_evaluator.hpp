@@ -198,6 +198,7 @@ public:
             Shard &sh = shards_[k];
             sh.items = std::make_unique<BatchItem<D>[]>(r);
             sh.meta = std::make_unique<Meta[]>(r);
+            sh.t_ns = std::make_unique<std::int64_t[]>(r);  // value-initialised: 0
             for (std::size_t i = 0; i < r; ++i)
                 sh.meta[i].seq.store(i, std::memory_order_relaxed);
         }
@@ -380,7 +381,6 @@ public:
 private:
     struct Meta {
         std::atomic<std::uint64_t> seq{0}; // == pos: free for lap pos; == pos+1: published
-        std::int64_t t_ns = 0;             // timeout > 0: time this item became its shard's head (0: not yet)
         TicketSlot *raw = nullptr;         // submit_slot(): resolve here instead of the item's ticket
     };
     struct Shard {
@@ -389,6 +389,9 @@ private:
         alignas(64) std::atomic<std::uint64_t> head{0}; // next position agents claim
         std::unique_ptr<BatchItem<D>[]> items;
         std::unique_ptr<Meta[]> meta;
+        // timeout > 0: time the item became its shard's head (0: not yet); kept
+        // out of Meta (16 B) since only range heads are ever stamped
+        std::unique_ptr<std::int64_t[]> t_ns;
         std::unique_ptr<unsigned char[]> packed;  // pre-packing backends: pb_ bytes per slot
     };
     struct Range {
@@ -435,7 +438,8 @@ private:
             }
             m.raw = raws[i];
             if (timeout_us_ > 0)
-                m.t_ns = sh.head.load(std::memory_order_relaxed) == pos ? ring_detail::now_ns() : 0;
+                if (sh.head.load(std::memory_order_relaxed) == pos)
+                    sh.t_ns[pos & mask_] = ring_detail::now_ns();
             if (i + 1 < n)
                 m.seq.store(pos + 1, std::memory_order_release);
             else
@@ -477,7 +481,8 @@ private:
         // head (as the reference restarts its clock after a full batch), which
         // keeps a clock read off almost every submit
         if (timeout_us_ > 0)
-            m.t_ns = sh.head.load(std::memory_order_relaxed) == pos ? ring_detail::now_ns() : 0;
+            if (sh.head.load(std::memory_order_relaxed) == pos)
+                sh.t_ns[pos & mask_] = ring_detail::now_ns();
         m.seq.store(pos + 1, std::memory_order_seq_cst);
         sh.inflight.fetch_sub(1, std::memory_order_release);
         const std::uint64_t depth = pos + 1 - sh.head.load(std::memory_order_seq_cst);
@@ -568,10 +573,10 @@ private:
                     ranges.push_back({k, h, c});
                     n += c;
                     if (timeout_us_ > 0) {
-                        Meta &hm = sh.meta[h & mask_];  // published: its producer is done with it
-                        if (hm.t_ns == 0)
-                            hm.t_ns = ring_detail::now_ns();
-                        oldest = std::min(oldest, hm.t_ns);
+                        std::int64_t &ht = sh.t_ns[h & mask_];  // published: its producer is done with it
+                        if (ht == 0)
+                            ht = ring_detail::now_ns();
+                        oldest = std::min(oldest, ht);
                     }
                 }
             }
@@ -764,6 +769,7 @@ private:
                 if (!it.features.empty())
                     FeatureVector().swap(it.features);
             }
+            sh.t_ns[r.h & mask_] = 0;  // only a range's head can carry a stamp
             for (std::size_t i = 0; i < r.n; ++i)
                 sh.meta[(r.h + i) & mask_].seq.store(r.h + i + ring_size_, std::memory_order_release);
         }
