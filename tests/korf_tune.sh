@@ -15,6 +15,6 @@ EXTRACT="import json,sys; r=json.loads(sys.stdin.readline()); print(json.dumps({
 for cfg in ${KORF_CFGS:-2_64_20_16 4_64_20_16 2_128_20_16 2_256_20_16 4_256_20_16 2_64_10_16 2_64_40_16 4_128_10_14 2_128_10_14 6_128_10_12}; do
   IFS=_ read a wn to th <<< "$cfg"
   BIDA_EVAL_AGENTS=$a BIDA_EVAL_SHARDS=16 timeout 300 tools/bin/bida_search_fast --domain stp4 --instances /tmp/bida_korf10.txt \
-    --model linear:/tmp/bida_man4.blin --q 0.5 --first 5 --count 1 --threads $th --mode gpu --work-num $wn --batch 8192 \
-    --timeout-us $to --d-init 14 --time-limit 120 | python -c "$EXTRACT" | sed "s/^{/{\"agents\": $a, \"work_num\": $wn, \"timeout_us\": $to, \"threads\": $th, /" >> gpurun_out/korf_tune.jsonl
+    --model linear:/tmp/bida_man4.blin --q 0.5 --first ${KORF_FIRST:-5} --count 1 --threads $th --mode gpu --work-num $wn --batch 8192 \
+    --timeout-us $to --d-init 14 --time-limit 120 | python -c "$EXTRACT" | sed "s/^{/{\"first\": ${KORF_FIRST:-5}, \"agents\": $a, \"work_num\": $wn, \"timeout_us\": $to, \"threads\": $th, /" >> gpurun_out/korf_tune.jsonl
 done
