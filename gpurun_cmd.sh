@@ -1,6 +1,10 @@
 #!/bin/bash
 cd "$(dirname "$0")"
 mkdir -p gpurun_out
-timeout 900 python bench.py > gpurun_out/r2_bench11.json 2> gpurun_out/r2_bench11.err
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r2_gputests_full7.log 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke5.log 2>&1
+rm -f gpurun_out/mlp_ab.jsonl
+for rep in 1 2; do
+  BIDA_GPU_LIB=paper_2507_11916_b200/_lib/libbida_gpu_old.so timeout 300 python tests/mlp_ab.py --tag old --models "128,128;128,128,128;160,96;256" >> gpurun_out/mlp_ab.jsonl 2>> gpurun_out/mlp_ab.err
+  BIDA_MLP_CM24=0 timeout 300 python tests/mlp_ab.py --tag cm32 --models "128,128;128,128,128;160,96;256" >> gpurun_out/mlp_ab.jsonl 2>> gpurun_out/mlp_ab.err
+  timeout 300 python tests/mlp_ab.py --tag cm24 --models "128,128;128,128,128;160,96;256" >> gpurun_out/mlp_ab.jsonl 2>> gpurun_out/mlp_ab.err
+done
+timeout 900 python -m pytest tests/test_gpu_mlp.py tests/test_mlp_pinned.py -q -x > gpurun_out/cm24_tests.log 2>&1

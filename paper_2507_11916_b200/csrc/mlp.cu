@@ -631,9 +631,10 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                     } else {
                         if (reader) {
                             // output layer: exact integer logits -> certified readout
-                            int32_t v[CM];
+                            constexpr int CV = (CM + 15) / 16 * 16;  // whole 16-column TMEM loads
+                            int32_t v[CV];
 #pragma unroll
-                            for (int c0 = 0; c0 < CM; c0 += 16) {
+                            for (int c0 = 0; c0 < CV; c0 += 16) {
                                 if (c0 < p.C) {
                                     int32_t r[16];
                                     sm100::tmem_ld16(t_row + c0, r);
@@ -664,7 +665,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                             }
                             bool fb = false;
                             const int h =
-                                readout_certified<CM>(v, p.C, p.scale_f[e], p.scale_d[e], p.rk, &dist_bad, &fb);
+                                readout_certified<CM>(reinterpret_cast<const int32_t(&)[CM]>(v), p.C, p.scale_f[e],
+                                                      p.scale_d[e], p.rk, &dist_bad, &fb);
                             if (fb && p.replays)
                                 atomicAdd(p.replays, 1ull);
                             hmin = min(hmin, h);
@@ -1158,8 +1160,13 @@ uint32_t rd32(const unsigned char *b) {
 
 template <int DOMAIN, int CM>
 int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
-    auto kern = p.mode != kWide ? mlp_fused_kernel<DOMAIN, CM>
-                : (p.cluster == 2 ? mlp_wide_kernel<DOMAIN, CM, true> : mlp_wide_kernel<DOMAIN, CM, false>);
+    auto kern = [&] {
+        if constexpr (CM == 24)  // fused schedules only (mlp_create)
+            return mlp_fused_kernel<DOMAIN, 24>;
+        else
+            return p.mode != kWide ? mlp_fused_kernel<DOMAIN, CM>
+                                   : (p.cluster == 2 ? mlp_wide_kernel<DOMAIN, CM, true> : mlp_wide_kernel<DOMAIN, CM, false>);
+    }();
     const int threads = kMlpThreads;
     std::call_once(m->attr_once, [&] {
         m->attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1221,6 +1228,7 @@ int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
 template <int DOMAIN>
 int launch_d(MlpModel *m, const MlpParams &p, cudaStream_t st) {
     switch (m->cm) {
+    case 24: return launch_t<DOMAIN, 24>(m, p, st);
     case 32: return launch_t<DOMAIN, 32>(m, p, st);
     case 64: return launch_t<DOMAIN, 64>(m, p, st);
     default: return launch_t<DOMAIN, 256>(m, p, st);
@@ -1538,6 +1546,10 @@ int mlp_create(const unsigned char *b, size_t len, int F, double thr, int num_sm
     if (p.mode != kWide)
         p.cluster = ((p.mode == kPair || p.mode == kSplit) && mcv && mcv[0] == '1') ? 2 : 1;
     m->cm = C <= 32 ? 32 : (C <= 64 ? 64 : 256);
+    // C <= 24 on a fused schedule: a 24-wide readout (BIDA_MLP_CM24=0: 32)
+    const char *c24 = std::getenv("BIDA_MLP_CM24");
+    if (C <= 24 && p.mode != kWide && !(c24 && c24[0] == '0'))
+        m->cm = 24;
     m->grid_cap = num_sms;
     if (const char *mc = std::getenv("BIDA_MLP_MAX_CTAS"))  // tests: many tiles per CTA on small batches
         m->grid_cap = std::max(1, std::min(num_sms, std::atoi(mc)));
@@ -1624,6 +1636,7 @@ int prepare_t(MlpModel *m, const MlpParams &p, KernelLaunch *out) {
 template <int DOMAIN>
 int prepare_d(MlpModel *m, const MlpParams &p, KernelLaunch *out) {
     switch (m->cm) {
+    case 24: return prepare_t<DOMAIN, 24>(m, p, out);
     case 32: return prepare_t<DOMAIN, 32>(m, p, out);
     case 64: return prepare_t<DOMAIN, 64>(m, p, out);
     default: return prepare_t<DOMAIN, 256>(m, p, out);
