@@ -345,7 +345,7 @@ SEARCH_WALK = (14, 2508)   # (length, seed) for random_walk_instance (instance.h
 SEARCH_CORNERS = 8
 
 
-def search_command(impl, model, q, seconds, threads, gpus, evaluators, batch, timeout_us, walk):
+def search_command(impl, model, q, seconds, threads, gpus, evaluators, batch, timeout_us, walk, work_num=128):
     """argv of one Batch IDA* run (see search_leg).  GPU legs spread
     `evaluators` GpuBackends over `gpus` devices (evaluator e on device
     e % gpus, tools/bida_search.cpp) and route searcher thread tid to
@@ -356,7 +356,7 @@ def search_command(impl, model, q, seconds, threads, gpus, evaluators, batch, ti
            "cpu_pdb": "tools/bin/bida_search"}[impl]
     if impl in ("fast", "ring", "reference"):
         extra = ["--mode", "gpu", "--gpu-pdb", "--gpus", str(gpus), "--evaluators", str(evaluators),
-                 "--work-num", "128", "--batch", str(batch), "--timeout-us", str(timeout_us)]
+                 "--work-num", str(work_num), "--batch", str(batch), "--timeout-us", str(timeout_us)]
     elif impl == "cpu":
         extra = ["--mode", "cpu", "--immediate", "--work-num", "1"]
     else:
@@ -375,7 +375,7 @@ def search_plan(rank, world):
 
 
 def search_leg(wl, seconds, threads, impl="fast", gpus=1, evaluators=1, agents=4, shards=16, batch=16384,
-               timeout_us=25, walk=None):
+               timeout_us=None, walk=None, work_num=None):
     """Batch IDA* nodes/s (BASELINE metric, second half): the reference's own
     batch_idastar (search.hpp:101-237, unchanged) on one config-2 Rubik's
     scramble, the workload's BMLP1 network evaluated for every generated node,
@@ -399,7 +399,15 @@ def search_leg(wl, seconds, threads, impl="fast", gpus=1, evaluators=1, agents=4
     model = f"/tmp/bida_bench_{os.getpid()}.bmlp"
     with open(model, "wb") as f:
         f.write(make_bmlp1("rc", hidden=wl["H"], classes=wl["C"], ensemble=wl["E"], seed=2507))
-    cmd = search_command(impl, model, wl["q"], seconds, threads, gpus, evaluators, batch, timeout_us, (L, seed))
+    # subtrees per searcher thread and flush timeout: 256 open subtrees helps
+    # every GPU leg (profiles/r2_search_knobs.jsonl, r2_ring_knobs.jsonl); the
+    # fast path's best flush timeout is 15 us, the others keep 25 us
+    if work_num is None:
+        work_num = 256
+    if timeout_us is None:
+        timeout_us = 15 if impl == "fast" else 25
+    cmd = search_command(impl, model, wl["q"], seconds, threads, gpus, evaluators, batch, timeout_us, (L, seed),
+                         work_num=work_num)
     if not os.path.exists(cmd[0]):
         return {"unavailable": f"{cmd[0]} not built"}
     env = {**os.environ, "BIDA_EVAL_AGENTS": str(agents), "BIDA_EVAL_SHARDS": str(shards)}
