@@ -773,9 +773,10 @@ def main():
         # Batch IDA* nodes/s on all `world` GPUs from one host process (rank 0; one
         # evaluator per GPU, tid % E routing, batch_eval.hpp:398-400)
         threads = host_cores()
-        # host-core budget (profiles/r2_search_host_sweep.jsonl): up to 4 agent threads
-        # per GPU evaluator within half the cores, searcher threads on the rest
-        agents = max(1, min(4, (threads // 2) // world))
+        # host-core budget: up to 3 agent threads per GPU evaluator within half the
+        # cores, searcher threads on the rest (13 + 3 on 16 cores is the best split
+        # once the submitters pre-pack: profiles/r2_search_balance_256.jsonl)
+        agents = max(1, min(3, (threads // 2) // world))
         gpu_threads = max(threads // 2, threads - agents * world)
         plan = search_plan(rank, world)
         sr = search_leg(wl, args.search_seconds, gpu_threads, agents=agents, **plan)
