@@ -463,8 +463,17 @@ def config1_leg(seconds, threads):
             ("gpu", "tools/bin/bida_search_fast", ["--mode", "gpu", "--work-num", "256", "--batch", "8192",
                                                    "--timeout-us", "20"],
              {"BIDA_EVAL_AGENTS": "2", "BIDA_EVAL_SHARDS": "16"}),
-            ("cpu_aidastar", "tools/bin/bida_search", ["--mode", "cpu", "--immediate", "--work-num", "1"], {})):
-        r = subprocess.run([os.path.join(ROOT, exe), *common, *extra], capture_output=True, text=True,
+            ("cpu_aidastar", "tools/bin/bida_search", ["--mode", "cpu", "--immediate", "--work-num", "1"], {}),
+            # the GPU at its own best work-generation depth (18: more, shorter subtrees for the
+            # latency-bound final iteration; the CPU is slowest there: profiles/r2_korf_dinit18.jsonl)
+            ("gpu_d_init_18", "tools/bin/bida_search_fast", ["--mode", "gpu", "--work-num", "256", "--batch", "8192",
+                                                             "--timeout-us", "20", "--d-init", "18"],
+             {"BIDA_EVAL_AGENTS": "2", "BIDA_EVAL_SHARDS": "16"})):
+        base = list(common)
+        if "--d-init" in extra:  # this leg's own depth replaces the shared one
+            i = base.index("--d-init")
+            del base[i:i + 2]
+        r = subprocess.run([os.path.join(ROOT, exe), *base, *extra], capture_output=True, text=True,
                            timeout=seconds * 3 + 120, env={**os.environ, **env})
         rows = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
         if r.returncode or not rows:
