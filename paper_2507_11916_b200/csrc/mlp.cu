@@ -263,11 +263,13 @@ __device__ __forceinline__ void requant_pipelined(uint32_t t_row, const int32_t 
 //               groups split hidden columns; group 1 encodes job j+1 while
 //               group 0 reads out job j, and TMEM is double-buffered by job
 //               parity so job j+1's MMAs overlap job j's readout.
-template <int DOMAIN, int CM>
+// RES: the resident schedule as a compile-time constant (its instantiation
+// drops the pair/split branches from the hot loops); RES = false reads p.mode.
+template <int DOMAIN, int CM, bool RES = false>
 __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_constant__ MlpParams p) {
     using T = DomainTraits<DOMAIN>;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int mode = p.mode;
+    const int mode = RES ? static_cast<int>(kResident) : p.mode;
     const int nsets = mode == kPair ? 2 : 1;  // activation buffer sets
     const int set_bytes = p.xbytes + p.ybytes;
     uint8_t *wbuf = smem + nsets * set_bytes;  // ring stages or resident image
@@ -1162,7 +1164,11 @@ template <int DOMAIN, int CM>
 int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
     auto kern = [&] {
         if constexpr (CM == 24)  // fused schedules only (mlp_create)
-            return mlp_fused_kernel<DOMAIN, 24>;
+            return p.mode == kResident ? mlp_fused_kernel<DOMAIN, 24, true> : mlp_fused_kernel<DOMAIN, 24>;
+        else if constexpr (CM <= 64)
+            return p.mode == kResident ? mlp_fused_kernel<DOMAIN, CM, true>
+                   : p.mode != kWide   ? mlp_fused_kernel<DOMAIN, CM>
+                   : (p.cluster == 2 ? mlp_wide_kernel<DOMAIN, CM, true> : mlp_wide_kernel<DOMAIN, CM, false>);
         else
             return p.mode != kWide ? mlp_fused_kernel<DOMAIN, CM>
                                    : (p.cluster == 2 ? mlp_wide_kernel<DOMAIN, CM, true> : mlp_wide_kernel<DOMAIN, CM, false>);
@@ -1618,7 +1624,12 @@ int mlp_launch(MlpModel *m, int domain, const void *d_packed, int64_t n, int32_t
 namespace {
 template <int DOMAIN, int CM>
 int prepare_t(MlpModel *m, const MlpParams &p, KernelLaunch *out) {
-    auto kern = mlp_fused_kernel<DOMAIN, CM>;
+    auto kern = [&] {
+        if constexpr (CM <= 64)
+            return p.mode == kResident ? mlp_fused_kernel<DOMAIN, CM, true> : mlp_fused_kernel<DOMAIN, CM>;
+        else
+            return mlp_fused_kernel<DOMAIN, CM>;
+    }();
     std::call_once(m->attr_once, [&] {
         m->attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(m->smem));
