@@ -263,13 +263,16 @@ __device__ __forceinline__ void requant_pipelined(uint32_t t_row, const int32_t 
 //               groups split hidden columns; group 1 encodes job j+1 while
 //               group 0 reads out job j, and TMEM is double-buffered by job
 //               parity so job j+1's MMAs overlap job j's readout.
-// RES: the resident schedule as a compile-time constant (its instantiation
-// drops the pair/split branches from the hot loops); RES = false reads p.mode.
-template <int DOMAIN, int CM, bool RES = false>
+// VAR: 0 reads the schedule from p.mode; 1 compiles the resident schedule in
+// as a constant (the pair/split branches drop out of the hot loops); 2 is
+// resident with folded biases and one ensemble member (the common case).
+template <int DOMAIN, int CM, int VAR = 0>
 __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_constant__ MlpParams p) {
     using T = DomainTraits<DOMAIN>;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int mode = RES ? static_cast<int>(kResident) : p.mode;
+    const int mode = VAR >= 1 ? static_cast<int>(kResident) : p.mode;
+    const int nE = VAR == 2 ? 1 : p.E;
+    const bool bfold = VAR == 2 ? true : p.bias_fold != 0;
     const int nsets = mode == kPair ? 2 : 1;  // activation buffer sets
     const int set_bytes = p.xbytes + p.ybytes;
     uint8_t *wbuf = smem + nsets * set_bytes;  // ring stages or resident image
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                 int s = 0;
                 uint32_t ph = 0, g = 0;  // g: global stage counter (multicast: CTA g%2 issues)
                 for (long long k0 = 0; k0 < nloc; k0 += per)
-                    for (int e = 0; e < p.E; ++e)
+                    for (int e = 0; e < nE; ++e)
                         for (int l = 0; l < p.nl; ++l)
                             for (int sl = 0; sl < per && k0 + sl < nloc; ++sl) {
                                 const MlpLayer &ly = p.layer[e][l];
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             uint32_t ph = 0, aph[2] = {0u, 0u};
             const uint32_t sbase = sm100::smem_u32(smem), sW = sm100::smem_u32(wbuf);
             for (long long k0 = 0; k0 < nloc; ++k0)
-                for (int e = 0; e < p.E; ++e) {
+                for (int e = 0; e < nE; ++e) {
                     int prev_half = 0;  // columns group 0 drained in the previous layer (0 = none)
                     for (int l = 0; l < p.nl; ++l) {
                         const MlpLayer ly = p.layer[e][l];
@@ -446,7 +449,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             const int per = mode == kPair ? 2 : 1;
             long long job = 0;
             for (long long k0 = 0; k0 < nloc; k0 += per)
-                for (int e = 0; e < p.E; ++e, ++job)
+                for (int e = 0; e < nE; ++e, ++job)
                     for (int l = 0; l < p.nl; ++l) {
                         const MlpLayer ly = p.layer[e][l];  // one copy per layer, not per MMA
                         const int nch = ly.K / kKChunk;
@@ -472,7 +475,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                 tmem + (mode == kPair ? sl * 256u : (mode == kResident && tdbl ? (job & 1) * 256u : 0u));
                             // descriptor of k-step 0; k-step i adds i*4096 B (A) / i*cbytes (B)
                             uint64_t adesc = sm100::make_smem_desc(abase, 2048u, 128u);
-                            const bool fold = mode == kResident && p.bias_fold;
+                            const bool fold = mode == kResident && bfold;
                             if (fold && sm100::elect_one())  // D = bias (digits x constant A), then += X.W
                                 sm100::mma_i8(dcol, sm100::make_smem_desc(sW + static_cast<uint32_t>(p.cA_off), 2048u, 128u),
                                               sm100::make_smem_desc(sW + static_cast<uint32_t>(ly.woff) + nch * cbytes,
@@ -578,7 +581,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
         load_state(kfirst, nlo, nhi);
         if (mode == kResident && encoder && nloc > 0)  // first job's one-hot
             encode(nlo, nhi, tile_valid(kfirst) && !state_bad(nlo, nhi), x_ready);
-        long long job = kfirst * p.E;
+        long long job = kfirst * nE;
         for (long long k = kfirst; k < nloc; k += kstep) {
             const long long st = (blockIdx.x + k * gridDim.x) * kTileM + row;
             const bool valid = st < p.n;
@@ -595,13 +598,13 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             int hmin = 0x7fffffff;
             bool dist_bad = false;
             tr(86);
-            for (int e = 0; e < p.E; ++e, ++job) {
+            for (int e = 0; e < nE; ++e, ++job) {
                 const uint32_t tcol = mode == kPair ? sl * 256u : (mode == kResident && tdbl ? (job & 1) * 256u : 0u);
                 const uint32_t t_row = tmem + tcol + (static_cast<uint32_t>(quad * 32) << 16);
                 if (mode != kResident) {
                     if (encoder)
                         encode(lo, hi, live, my_ready);
-                    else if (mode != kSplit || job == kfirst * p.E)
+                    else if (mode != kSplit || job == kfirst * nE)
                         sm100::mbar_arrive(my_ready);  // split: later jobs arrive at the previous readout
                 }
                 for (int l = 0; l < p.nl; ++l) {
@@ -622,7 +625,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                         const uint32_t out = ((l + 1) & 1) ? sY : sX;
                         const int half = mode == kPair ? ly.N : ly.N / 2;
                         const int c_beg = mode == kPair ? 0 : grp * half, c_end = c_beg + half;
-                        if (p.bias_fold)
+                        if (bfold)
                             requant_pipelined<false>(t_row, bias, ly.shift, out, row, c_beg, c_end);
                         else
                             requant_pipelined<true>(t_row, bias, ly.shift, out, row, c_beg, c_end);
@@ -641,7 +644,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                     int32_t r[16];
                                     sm100::tmem_ld16(t_row + c0, r);
                                     int4 b4[4] = {};
-                                    if (!p.bias_fold) {
+                                    if (!bfold) {
 #pragma unroll
                                         for (int q = 0; q < 4; ++q)
                                             b4[q] = __ldg(reinterpret_cast<const int4 *>(bias + c0) + q);
@@ -657,11 +660,11 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                 }
                             }
                             sm100::tc_fence_before();
-                            if (mode == kSplit && (e + 1 < p.E || k + 1 < nloc))
+                            if (mode == kSplit && (e + 1 < nE || k + 1 < nloc))
                                 sm100::mbar_arrive(my_ready);  // TMEM free: next job's layer 0 may start
                             tr(81);
                             if (p.logits_out && valid) {
-                                double *dst = p.logits_out + (static_cast<size_t>(st) * p.E + e) * p.C;
+                                double *dst = p.logits_out + (static_cast<size_t>(st) * nE + e) * p.C;
                                 for (int c = 0; c < p.C; ++c)
                                     dst[c] = static_cast<double>(v[c]) * p.scale_d[e];
                             }
@@ -677,7 +680,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                         }
                         if (mode == kResident && encoder) {
                             // next job's one-hot: X is free once this job's last layer completed
-                            const bool last_member = e + 1 == p.E;
+                            const bool last_member = e + 1 == nE;
                             const long long kn = last_member ? k + 1 : k;
                             if (kn < nloc) {
                                 const uint64_t elo = last_member ? nlo : lo, ehi = last_member ? nhi : hi;
@@ -1164,9 +1167,10 @@ template <int DOMAIN, int CM>
 int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
     auto kern = [&] {
         if constexpr (CM == 24)  // fused schedules only (mlp_create)
-            return p.mode == kResident ? mlp_fused_kernel<DOMAIN, 24, true> : mlp_fused_kernel<DOMAIN, 24>;
+            return p.mode == kResident ? (p.bias_fold && p.E == 1 ? mlp_fused_kernel<DOMAIN, 24, 2> : mlp_fused_kernel<DOMAIN, 24, 1>)
+                                       : mlp_fused_kernel<DOMAIN, 24>;
         else if constexpr (CM <= 64)
-            return p.mode == kResident ? mlp_fused_kernel<DOMAIN, CM, true>
+            return p.mode == kResident ? (p.bias_fold && p.E == 1 ? mlp_fused_kernel<DOMAIN, CM, 2> : mlp_fused_kernel<DOMAIN, CM, 1>)
                    : p.mode != kWide   ? mlp_fused_kernel<DOMAIN, CM>
                    : (p.cluster == 2 ? mlp_wide_kernel<DOMAIN, CM, true> : mlp_wide_kernel<DOMAIN, CM, false>);
         else
@@ -1626,7 +1630,8 @@ template <int DOMAIN, int CM>
 int prepare_t(MlpModel *m, const MlpParams &p, KernelLaunch *out) {
     auto kern = [&] {
         if constexpr (CM <= 64)
-            return p.mode == kResident ? mlp_fused_kernel<DOMAIN, CM, true> : mlp_fused_kernel<DOMAIN, CM>;
+            return p.mode == kResident ? (p.bias_fold && p.E == 1 ? mlp_fused_kernel<DOMAIN, CM, 2> : mlp_fused_kernel<DOMAIN, CM, 1>)
+                                       : mlp_fused_kernel<DOMAIN, CM>;
         else
             return mlp_fused_kernel<DOMAIN, CM>;
     }();
