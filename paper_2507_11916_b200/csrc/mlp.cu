@@ -265,14 +265,16 @@ __device__ __forceinline__ void requant_pipelined(uint32_t t_row, const int32_t 
 //               parity so job j+1's MMAs overlap job j's readout.
 // VAR: 0 reads the schedule from p.mode; 1 compiles the resident schedule in
 // as a constant (the pair/split branches drop out of the hot loops); 2 is
-// resident with folded biases and one ensemble member (the common case).
+// resident with folded biases and one ensemble member (the common case); 3
+// adds a fixed depth of two hidden layers.
 template <int DOMAIN, int CM, int VAR = 0>
 __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_constant__ MlpParams p) {
     using T = DomainTraits<DOMAIN>;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int mode = VAR >= 1 ? static_cast<int>(kResident) : p.mode;
-    const int nE = VAR == 2 ? 1 : p.E;
-    const bool bfold = VAR == 2 ? true : p.bias_fold != 0;
+    const int nE = VAR >= 2 ? 1 : p.E;
+    const bool bfold = VAR >= 2 ? true : p.bias_fold != 0;
+    const int nL = VAR == 3 ? 3 : p.nl;  // 3: two hidden layers + the output layer
     const int nsets = mode == kPair ? 2 : 1;  // activation buffer sets
     const int set_bytes = p.xbytes + p.ybytes;
     uint8_t *wbuf = smem + nsets * set_bytes;  // ring stages or resident image
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                 uint32_t ph = 0, g = 0;  // g: global stage counter (multicast: CTA g%2 issues)
                 for (long long k0 = 0; k0 < nloc; k0 += per)
                     for (int e = 0; e < nE; ++e)
-                        for (int l = 0; l < p.nl; ++l)
+                        for (int l = 0; l < nL; ++l)
                             for (int sl = 0; sl < per && k0 + sl < nloc; ++sl) {
                                 const MlpLayer &ly = p.layer[e][l];
                                 const int nch = ly.K / kKChunk, cps = ly.cps;
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             for (long long k0 = 0; k0 < nloc; ++k0)
                 for (int e = 0; e < nE; ++e) {
                     int prev_half = 0;  // columns group 0 drained in the previous layer (0 = none)
-                    for (int l = 0; l < p.nl; ++l) {
+                    for (int l = 0; l < nL; ++l) {
                         const MlpLayer ly = p.layer[e][l];
                         const int nch = ly.K / kKChunk, cps = ly.cps, Nh = ly.N / ly.nh;
                         const uint32_t cbytes = static_cast<uint32_t>(Nh) * kKChunk;
@@ -432,7 +434,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                                 }
                             }
                             if (sm100::elect_one())
-                                sm100::mma_commit(l + 1 < p.nl ? &d_full[h] : o_full);
+                                sm100::mma_commit(l + 1 < nL ? &d_full[h] : o_full);
                             __syncwarp();
                         }
                         if (lane_id() == 0)
@@ -450,7 +452,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
             long long job = 0;
             for (long long k0 = 0; k0 < nloc; k0 += per)
                 for (int e = 0; e < nE; ++e, ++job)
-                    for (int l = 0; l < p.nl; ++l) {
+                    for (int l = 0; l < nL; ++l) {
                         const MlpLayer ly = p.layer[e][l];  // one copy per layer, not per MMA
                         const int nch = ly.K / kKChunk;
                         const int cps = mode == kResident ? nch : ly.cps;
@@ -607,10 +609,10 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                     else if (mode != kSplit || job == kfirst * nE)
                         sm100::mbar_arrive(my_ready);  // split: later jobs arrive at the previous readout
                 }
-                for (int l = 0; l < p.nl; ++l) {
+                for (int l = 0; l < nL; ++l) {
                     const MlpLayer &ly = p.layer[e][l];
                     tr(50 + l);
-                    if (mode == kSplit && l + 1 == p.nl) {
+                    if (mode == kSplit && l + 1 == nL) {
                         sm100::mbar_wait(o_full, oph);
                         oph ^= 1u;
                     } else {
@@ -620,7 +622,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_fused_kernel(const __grid_
                     tr(60 + l);
                     sm100::tc_fence_after();
                     const int32_t *bias = p.bias + ly.boff;
-                    if (l + 1 < p.nl) {
+                    if (l + 1 < nL) {
                         // hidden layer epilogue: (acc + bias) >> shift -> u8 A operand of layer l+1
                         const uint32_t out = ((l + 1) & 1) ? sY : sX;
                         const int half = mode == kPair ? ly.N : ly.N / 2;
@@ -1167,10 +1169,12 @@ template <int DOMAIN, int CM>
 int launch_t(MlpModel *m, const MlpParams &p, cudaStream_t st) {
     auto kern = [&] {
         if constexpr (CM == 24)  // fused schedules only (mlp_create)
-            return p.mode == kResident ? (p.bias_fold && p.E == 1 ? mlp_fused_kernel<DOMAIN, 24, 2> : mlp_fused_kernel<DOMAIN, 24, 1>)
+            return p.mode == kResident ? (p.bias_fold && p.E == 1 ? (p.nl == 3 ? mlp_fused_kernel<DOMAIN, 24, 3> : mlp_fused_kernel<DOMAIN, 24, 2>)
+                                                                   : mlp_fused_kernel<DOMAIN, 24, 1>)
                                        : mlp_fused_kernel<DOMAIN, 24>;
         else if constexpr (CM <= 64)
-            return p.mode == kResident ? (p.bias_fold && p.E == 1 ? mlp_fused_kernel<DOMAIN, CM, 2> : mlp_fused_kernel<DOMAIN, CM, 1>)
+            return p.mode == kResident ? (p.bias_fold && p.E == 1 ? (p.nl == 3 ? mlp_fused_kernel<DOMAIN, CM, 3> : mlp_fused_kernel<DOMAIN, CM, 2>)
+                                                                   : mlp_fused_kernel<DOMAIN, CM, 1>)
                    : p.mode != kWide   ? mlp_fused_kernel<DOMAIN, CM>
                    : (p.cluster == 2 ? mlp_wide_kernel<DOMAIN, CM, true> : mlp_wide_kernel<DOMAIN, CM, false>);
         else
@@ -1630,7 +1634,8 @@ template <int DOMAIN, int CM>
 int prepare_t(MlpModel *m, const MlpParams &p, KernelLaunch *out) {
     auto kern = [&] {
         if constexpr (CM <= 64)
-            return p.mode == kResident ? (p.bias_fold && p.E == 1 ? mlp_fused_kernel<DOMAIN, CM, 2> : mlp_fused_kernel<DOMAIN, CM, 1>)
+            return p.mode == kResident ? (p.bias_fold && p.E == 1 ? (p.nl == 3 ? mlp_fused_kernel<DOMAIN, CM, 3> : mlp_fused_kernel<DOMAIN, CM, 2>)
+                                                                   : mlp_fused_kernel<DOMAIN, CM, 1>)
                                        : mlp_fused_kernel<DOMAIN, CM>;
         else
             return mlp_fused_kernel<DOMAIN, CM>;
