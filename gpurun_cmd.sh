@@ -1,11 +1,9 @@
 #!/bin/bash
 cd "$(dirname "$0")"
 mkdir -p gpurun_out
-timeout 900 python bench.py > gpurun_out/r2_bench15.json 2> gpurun_out/r2_bench15.err
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r2_gputests_full9.log 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke7.log 2>&1
-python tests/profile_kernel.py --model mlp --hidden 128,128 --n 1048576 --launches 2 > gpurun_out/prof_plain.log 2>&1 && \
-ncu --set full --import-source on --clock-control none -k regex:mlp_fused -s 1 -c 1 -o gpurun_out/r2_h128_v4 -f \
-  python tests/profile_kernel.py --model mlp --hidden 128,128 --n 1048576 --launches 2 > gpurun_out/ncu_v4.log 2>&1
-B="python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-wide-leg --no-linear-leg --no-sweep --search-seconds 0"
-$B > gpurun_out/launch_plain.json 2> gpurun_out/launch_plain.err && ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_default_r2d.csv $B > gpurun_out/ncu_launch.log 2>&1
+rm -f gpurun_out/mlp_ab.jsonl
+for rep in 1 2; do
+  BIDA_GPU_LIB=paper_2507_11916_b200/_lib/libbida_gpu_old.so timeout 300 python tests/mlp_ab.py --tag old --models "1610,1610;512,512" --n 2097152 --check 4096 >> gpurun_out/mlp_ab.jsonl 2>> gpurun_out/mlp_ab.err
+  timeout 300 python tests/mlp_ab.py --tag fix3 --models "1610,1610;512,512" --n 2097152 --check 4096 >> gpurun_out/mlp_ab.jsonl 2>> gpurun_out/mlp_ab.err
+done
+timeout 900 python -m pytest tests/test_gpu_mlp.py -q -x -k "wide" > gpurun_out/wide_tests.log 2>&1
