@@ -460,19 +460,23 @@ def config1_leg(seconds, threads):
               "--count", "1", "--threads", str(threads), "--d-init", str(d_init), "--time-limit", str(seconds)]
     out = {}
     for side, exe, extra, env in (
+            # GPU sides: 2 agents + cores - 2 searcher threads, 10 us flush timeout
+            # (tests/korf_tune.sh, profiles/r2_korf_tune_final.jsonl)
             ("gpu", "tools/bin/bida_search_fast", ["--mode", "gpu", "--work-num", "256", "--batch", "8192",
-                                                   "--timeout-us", "20"],
+                                                   "--timeout-us", "10", "--threads", str(max(1, threads - 2))],
              {"BIDA_EVAL_AGENTS": "2", "BIDA_EVAL_SHARDS": "16"}),
             ("cpu_aidastar", "tools/bin/bida_search", ["--mode", "cpu", "--immediate", "--work-num", "1"], {}),
             # the GPU at its own best work-generation depth (18: more, shorter subtrees for the
             # latency-bound final iteration; the CPU is slowest there: profiles/r2_korf_dinit18.jsonl)
             ("gpu_d_init_18", "tools/bin/bida_search_fast", ["--mode", "gpu", "--work-num", "256", "--batch", "8192",
-                                                             "--timeout-us", "20", "--d-init", "18"],
+                                                             "--timeout-us", "10", "--threads", str(max(1, threads - 2)),
+                                                             "--d-init", "18"],
              {"BIDA_EVAL_AGENTS": "2", "BIDA_EVAL_SHARDS": "16"})):
         base = list(common)
-        if "--d-init" in extra:  # this leg's own depth replaces the shared one
-            i = base.index("--d-init")
-            del base[i:i + 2]
+        for flag in ("--d-init", "--threads"):  # this leg's own setting replaces the shared one
+            if flag in extra:
+                i = base.index(flag)
+                del base[i:i + 2]
         r = subprocess.run([os.path.join(ROOT, exe), *base, *extra], capture_output=True, text=True,
                            timeout=seconds * 3 + 120, env={**os.environ, **env})
         rows = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
